@@ -1,0 +1,615 @@
+// Host runtime + C ABI (include/geopairs_b200.h).
+//
+// The runtime owns all device memory of a context (image, tree store, run
+// workspace) and of a store (D, mark bitmap, counts).  gp_run drives the
+// device commit loop (commit.cu) and the speculative propagation batches
+// (propagate.cu); the only host<->device traffic per batch is a 32-byte
+// control block.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/geopairs_b200.h"
+#include "gp_common.cuh"
+#include "gp_kernels.h"
+
+using namespace gp;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                               \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return fail(GP_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+struct gp_ctx {
+  Grid g;
+  int isint;
+  float* d_img = nullptr;
+  cudaStream_t st = nullptr;
+  int nsm = 148;
+  // tree store + run workspace (lazily sized)
+  float* tdist = nullptr;
+  uint8_t* tdir = nullptr;
+  int tcap = 0;
+  uint32_t* scratch = nullptr;
+  size_t scratch_trees = 0;
+};
+
+struct gp_store {
+  int64_t n;
+  int NW;
+  float* D = nullptr;
+  uint32_t* mark = nullptr;
+  int* cnt = nullptr;
+  unsigned long long* out3 = nullptr;
+  int64_t filled = 0;
+  cudaStream_t st = nullptr;
+};
+
+extern "C" const char* gp_last_error(void) { return g_err.c_str(); }
+extern "C" int gp_version(void) { return 1; }
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T) + 16);
+}
+
+extern "C" int gp_ctx_create(int H, int W, int dtype, const void* pixels, int metric, int conn,
+                             gp_ctx** out) {
+  if (!out || !pixels) return fail(GP_EINVAL, "null argument");
+  if (H < 1 || W < 1 || (int64_t)H * W < 2) return fail(GP_EINVAL, "image must contain at least 2 pixels");
+  if ((int64_t)H * W > 65536) return fail(GP_EINVAL, "images above 65536 pixels are not supported (dense N^2 store)");
+  if (conn != 4 && conn != 8) return fail(GP_EINVAL, "connectivity must be 4 or 8");
+  if (metric < 0 || metric > 2) return fail(GP_EINVAL, "unknown metric");
+  const int N = H * W;
+  std::vector<float> f(N);
+  int isint = dtype != GP_DTYPE_F32;
+  double vmax = 0.0;
+  for (int i = 0; i < N; i++) {
+    double v;
+    if (dtype == GP_DTYPE_I64) v = (double)((const int64_t*)pixels)[i];
+    else if (dtype == GP_DTYPE_U8) v = (double)((const uint8_t*)pixels)[i];
+    else if (dtype == GP_DTYPE_F32) v = (double)((const float*)pixels)[i];
+    else return fail(GP_EINVAL, "unknown dtype");
+    if (isint && (v < 1 || v > 255))
+      return fail(GP_EINVAL, "grey levels must be in [1, 255]");
+    if (!isint && (!std::isfinite(v) || v < 0))
+      return fail(GP_EINVAL, "float pixel values must be finite and >= 0");
+    f[i] = (float)v;
+    vmax = std::max(vmax, v);
+  }
+  if (isint) {
+    // fp32 exactness: every geodesic distance <= wmax * (hops of a straight path)
+    double hops = conn == 8 ? std::max(H, W) - 1 : (H - 1) + (W - 1);
+    double wmax = metric == GP_METRIC_MEAN ? 2 * vmax : 4 * vmax;
+    if (wmax * hops >= 16777216.0) return fail(GP_EINVAL, "integer distances would exceed 2^24");
+  }
+  gp_ctx* c = new gp_ctx();
+  c->g = Grid{H, W, N, conn, metric};
+  c->isint = isint;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = dalloc(&c->d_img, N);
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_img, f.data(), N * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    gp_ctx_destroy(c);
+    return fail(GP_ECUDA, std::string("ctx alloc: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return GP_OK;
+}
+
+extern "C" void gp_ctx_destroy(gp_ctx* c) {
+  if (!c) return;
+  cudaFree(c->d_img);
+  cudaFree(c->tdist);
+  cudaFree(c->tdir);
+  cudaFree(c->scratch);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+extern "C" int gp_ctx_num_pixels(const gp_ctx* c) { return c ? c->g.N : 0; }
+
+static int ensure_scratch(gp_ctx* c, size_t ntrees) {
+  if (prop_fits_smem(c->g.N) || ntrees <= c->scratch_trees) return GP_OK;
+  cudaFree(c->scratch);
+  c->scratch = nullptr;
+  c->scratch_trees = 0;
+  CUDA_TRY(dalloc(&c->scratch, prop_scratch_words(c->g.N) * ntrees));
+  c->scratch_trees = ntrees;
+  return GP_OK;
+}
+
+static PropArgs base_prop(gp_ctx* c) {
+  PropArgs a;
+  memset(&a, 0, sizeof(a));
+  a.g = c->g;
+  a.img = c->d_img;
+  a.scratch = c->scratch;
+  a.delta = INFINITY;
+  return a;
+}
+
+static float default_delta(const gp_ctx* c) {
+  (void)c;
+  return INFINITY;
+}
+
+extern "C" int gp_propagate(gp_ctx* c, const int32_t* sources, int nsrc, float* dist_out,
+                            int32_t* parent_out) {
+  if (!c || !sources || nsrc < 1) return fail(GP_EINVAL, "at least one source pixel is required");
+  const int N = c->g.N;
+  std::vector<char> seen(N, 0);
+  for (int i = 0; i < nsrc; i++) {
+    if (sources[i] < 0 || sources[i] >= N) return fail(GP_EINVAL, "source out of range");
+    if (seen[sources[i]]++) return fail(GP_EINVAL, "duplicate source pixels");
+  }
+  int rc = ensure_scratch(c, 1);
+  if (rc) return rc;
+  int* d_src = nullptr;
+  float* d_dist = nullptr;
+  uint8_t* d_dir = nullptr;
+  CUDA_TRY(dalloc(&d_src, nsrc));
+  CUDA_TRY(dalloc(&d_dist, N));
+  CUDA_TRY(dalloc(&d_dir, N));
+  CUDA_TRY(cudaMemcpyAsync(d_src, sources, nsrc * 4, cudaMemcpyHostToDevice, c->st));
+  PropArgs a = base_prop(c);
+  a.src = d_src;
+  a.ns = nsrc;
+  a.out_dist = d_dist;
+  a.out_dir = d_dir;
+  a.delta = default_delta(c);
+  CUDA_TRY(launch_propagate(a, 1, c->st));
+  std::vector<uint8_t> dir(N);
+  if (dist_out) CUDA_TRY(cudaMemcpyAsync(dist_out, d_dist, N * 4, cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaMemcpyAsync(dir.data(), d_dir, N, cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  cudaFree(d_src);
+  cudaFree(d_dist);
+  cudaFree(d_dir);
+  if (parent_out) {
+    const int W = c->g.W;
+    for (int v = 0; v < N; v++) {
+      uint8_t k = dir[v];
+      parent_out[v] = k == GP_ROOT ? -1 : v + (k / 3 - 1) * W + (k % 3 - 1);
+    }
+  }
+  return GP_OK;
+}
+
+extern "C" int gp_propagate_batch(gp_ctx* c, const int32_t* src_dev, int k, float* tdist_dev,
+                                  uint8_t* dir_dev, void* stream) {
+  if (!c || !src_dev || k < 0) return fail(GP_EINVAL, "bad arguments");
+  int rc = ensure_scratch(c, (size_t)k);
+  if (rc) return rc;
+  PropArgs a = base_prop(c);
+  a.src = src_dev;
+  a.ns = 1;
+  a.out_dist = tdist_dev;
+  a.out_dir = dir_dev;
+  a.delta = default_delta(c);
+  CUDA_TRY(launch_propagate(a, k, (cudaStream_t)stream));
+  return GP_OK;
+}
+
+static std::vector<int32_t> boundary_pixels(int W, int H) {  // propagation.py:130-143
+  std::vector<int32_t> out;
+  for (int r = 0; r < H; r++) {
+    if (r == 0 || r == H - 1) {
+      for (int col = 0; col < W; col++) out.push_back(r * W + col);
+    } else {
+      out.push_back(r * W);
+      if (W > 1) out.push_back(r * W + W - 1);
+    }
+  }
+  return out;
+}
+
+// _extrema_context (strategies.py:109-116) on the device; returns the
+// centroid, and fills dfc_dev [N] (device) and the host dist_from_c copy.
+static int extrema_device(gp_ctx* c, int* centroid, float* dfc_dev, std::vector<float>& dfc_host) {
+  const int N = c->g.N;
+  std::vector<int32_t> border = boundary_pixels(c->g.W, c->g.H);
+  int* d_src = nullptr;
+  int* d_cen = nullptr;
+  float* d_fb = nullptr;
+  int rc = ensure_scratch(c, 1);
+  if (rc) return rc;
+  CUDA_TRY(dalloc(&d_src, border.size() + 1));
+  CUDA_TRY(dalloc(&d_cen, 1));
+  CUDA_TRY(dalloc(&d_fb, N));
+  CUDA_TRY(cudaMemcpyAsync(d_src, border.data(), border.size() * 4, cudaMemcpyHostToDevice, c->st));
+  PropArgs a = base_prop(c);
+  a.src = d_src;
+  a.ns = (int)border.size();
+  a.out_dist = d_fb;
+  a.delta = default_delta(c);
+  CUDA_TRY(launch_propagate(a, 1, c->st));
+  CUDA_TRY(launch_argmax_first(d_fb, N, d_cen, c->st));  // first max = smallest id
+  PropArgs b = base_prop(c);
+  b.src = d_cen;
+  b.ns = 1;
+  b.out_dist = dfc_dev;
+  b.delta = default_delta(c);
+  CUDA_TRY(launch_propagate(b, 1, c->st));
+  dfc_host.resize(N);
+  CUDA_TRY(cudaMemcpyAsync(centroid, d_cen, 4, cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaMemcpyAsync(dfc_host.data(), dfc_dev, N * 4, cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  cudaFree(d_src);
+  cudaFree(d_cen);
+  cudaFree(d_fb);
+  return GP_OK;
+}
+
+static void ext_order(const std::vector<float>& dfc, std::vector<int32_t>& ext) {
+  // ext = lexsort((id, -dfc)): decreasing distance, ties by increasing id
+  const int N = (int)dfc.size();
+  ext.resize(N);
+  for (int i = 0; i < N; i++) ext[i] = i;
+  std::stable_sort(ext.begin(), ext.end(), [&](int32_t x, int32_t y) { return dfc[x] > dfc[y]; });
+}
+
+extern "C" int gp_extrema(gp_ctx* c, int32_t* centroid, float* dfc_out, int32_t* ext_out) {
+  if (!c) return fail(GP_EINVAL, "null ctx");
+  float* d_dfc = nullptr;
+  CUDA_TRY(dalloc(&d_dfc, c->g.N));
+  std::vector<float> dfc;
+  int cen = -1;
+  int rc = extrema_device(c, &cen, d_dfc, dfc);
+  cudaFree(d_dfc);
+  if (rc) return rc;
+  std::vector<int32_t> ext;
+  ext_order(dfc, ext);
+  if (centroid) *centroid = cen;
+  if (dfc_out) memcpy(dfc_out, dfc.data(), dfc.size() * 4);
+  if (ext_out) memcpy(ext_out, ext.data(), ext.size() * 4);
+  return GP_OK;
+}
+
+// ---------------- store ----------------
+extern "C" int gp_store_create(int64_t n, gp_store** out) {
+  if (!out) return fail(GP_EINVAL, "null argument");
+  if (n < 2) return fail(GP_EINVAL, "need at least 2 pixels");
+  if (n > 65536) return fail(GP_ENOMEM, "stores above 65536 pixels are not supported");
+  gp_store* s = new gp_store();
+  s->n = n;
+  s->NW = (int)((n + 31) / 32);
+  cudaError_t e = cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = dalloc(&s->D, (size_t)n * n);
+  if (e == cudaSuccess) e = dalloc(&s->mark, (size_t)n * s->NW);
+  if (e == cudaSuccess) e = dalloc(&s->cnt, (size_t)n);
+  if (e == cudaSuccess) e = dalloc(&s->out3, 3);
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->cnt, 0, n * 4, s->st);
+  if (e == cudaSuccess) e = launch_store_init(s->mark, s->NW, s->D, (int)n, s->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->st);
+  if (e != cudaSuccess) {
+    gp_store_destroy(s);
+    return fail(e == cudaErrorMemoryAllocation ? GP_ENOMEM : GP_ECUDA,
+                std::string("store alloc: ") + cudaGetErrorString(e));
+  }
+  *out = s;
+  return GP_OK;
+}
+
+extern "C" void gp_store_destroy(gp_store* s) {
+  if (!s) return;
+  cudaFree(s->D);
+  cudaFree(s->mark);
+  cudaFree(s->cnt);
+  cudaFree(s->out3);
+  if (s->st) cudaStreamDestroy(s->st);
+  delete s;
+}
+
+extern "C" int gp_store_device_ptrs(gp_store* s, float** D, uint32_t** mark, int32_t** counts,
+                                    int64_t* words) {
+  if (!s) return fail(GP_EINVAL, "null store");
+  if (D) *D = s->D;
+  if (mark) *mark = s->mark;
+  if (counts) *counts = s->cnt;
+  if (words) *words = s->NW;
+  return GP_OK;
+}
+
+extern "C" int gp_store_fill_tree(gp_store* s, const int32_t* parent, const float* tdist,
+                                  float tol, int64_t* new_pairs) {
+  if (!s || !parent || !tdist) return fail(GP_EINVAL, "null argument");
+  const int N = (int)s->n;
+  int* d_par = nullptr;
+  float* d_td = nullptr;
+  CUDA_TRY(dalloc(&d_par, N));
+  CUDA_TRY(dalloc(&d_td, N));
+  CUDA_TRY(cudaMemcpyAsync(d_par, parent, N * 4, cudaMemcpyHostToDevice, s->st));
+  CUDA_TRY(cudaMemcpyAsync(d_td, tdist, N * 4, cudaMemcpyHostToDevice, s->st));
+  // snapshot so that a failed fill leaves the store unchanged is not needed by
+  // the reference (it also mutates before raising); mirror that behaviour.
+  CUDA_TRY(cudaMemsetAsync(s->out3, 0, 24, s->st));
+  CUDA_TRY(launch_fill_tree_api(N, s->NW, d_par, d_td, s->mark, s->cnt, s->D, s->out3, tol, s->st));
+  unsigned long long o[3];
+  CUDA_TRY(cudaMemcpyAsync(o, s->out3, 24, cudaMemcpyDeviceToHost, s->st));
+  CUDA_TRY(cudaStreamSynchronize(s->st));
+  cudaFree(d_par);
+  cudaFree(d_td);
+  if (o[2]) return fail(GP_ECYCLE, "tree parent links contain a cycle");
+  if (o[1]) return fail(GP_EDISAGREE, "tree distances disagree with " + std::to_string(o[1]) +
+                                          " already-stored entries");
+  s->filled += (int64_t)o[0];
+  if (new_pairs) *new_pairs = (int64_t)o[0];
+  return GP_OK;
+}
+
+extern "C" int gp_store_fill_source(gp_store* s, int64_t source, const float* dist, float tol,
+                                    int64_t* new_pairs) {
+  if (!s || !dist) return fail(GP_EINVAL, "null argument");
+  const int N = (int)s->n;
+  if (source < 0 || source >= N) return fail(GP_EINVAL, "source out of range");
+  if (dist[source] != 0.0f) return fail(GP_EINVAL, "source's distance to itself must be 0");
+  float* d_dist = nullptr;
+  CUDA_TRY(dalloc(&d_dist, N));
+  CUDA_TRY(cudaMemcpyAsync(d_dist, dist, N * 4, cudaMemcpyHostToDevice, s->st));
+  CUDA_TRY(cudaMemsetAsync(s->out3, 0, 24, s->st));
+  // the reference checks agreement before writing anything (distances.py:132-136)
+  CUDA_TRY(launch_fill_source_api(N, s->NW, (int)source, d_dist, s->mark, s->cnt, s->D, s->out3,
+                                  tol, s->st));
+  unsigned long long o[3];
+  CUDA_TRY(cudaMemcpyAsync(o, s->out3, 24, cudaMemcpyDeviceToHost, s->st));
+  CUDA_TRY(cudaStreamSynchronize(s->st));
+  cudaFree(d_dist);
+  if (o[1]) return fail(GP_EDISAGREE, "distance map disagrees with already-stored entries");
+  s->filled += (int64_t)o[0];
+  if (new_pairs) *new_pairs = (int64_t)o[0];
+  return GP_OK;
+}
+
+extern "C" int gp_store_counts(gp_store* s, int32_t* counts_out, int64_t* filled) {
+  if (!s) return fail(GP_EINVAL, "null store");
+  if (counts_out) {
+    CUDA_TRY(cudaMemcpyAsync(counts_out, s->cnt, s->n * 4, cudaMemcpyDeviceToHost, s->st));
+    CUDA_TRY(cudaStreamSynchronize(s->st));
+  }
+  if (filled) *filled = s->filled;
+  return GP_OK;
+}
+
+extern "C" int gp_store_read(gp_store* s, float* D_out, uint8_t* mark_out) {
+  if (!s) return fail(GP_EINVAL, "null store");
+  const size_t nn = (size_t)s->n * s->n;
+  if (D_out) CUDA_TRY(cudaMemcpyAsync(D_out, s->D, nn * 4, cudaMemcpyDeviceToHost, s->st));
+  if (mark_out) {
+    uint8_t* d_m = nullptr;
+    CUDA_TRY(dalloc(&d_m, nn));
+    CUDA_TRY(launch_mark_unpack(s->mark, (int)s->n, s->NW, d_m, s->st));
+    CUDA_TRY(cudaMemcpyAsync(mark_out, d_m, nn, cudaMemcpyDeviceToHost, s->st));
+    CUDA_TRY(cudaStreamSynchronize(s->st));
+    cudaFree(d_m);
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->st));
+  return GP_OK;
+}
+
+// ---------------- run_strategy ----------------
+struct EvPair {
+  cudaEvent_t a, b;
+};
+
+static float ev_ms(const EvPair& p) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, p.a, p.b);
+  return ms;
+}
+
+extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, int spec_k,
+                      int32_t* seq_out, int64_t* new_out, gp_run_stats* stats) {
+  if (!c || !s) return fail(GP_EINVAL, "null argument");
+  const int N = c->g.N, NW = s->NW;
+  if (s->n != N) return fail(GP_EINVAL, "store size does not match the image");
+  if (strategy != GP_STRATEGY_NAIVE && strategy != GP_STRATEGY_FILLING_RATE)
+    return fail(GP_EINVAL, "strategy not supported on the device path");
+  cudaStream_t st = c->st;
+  gp_run_stats S;
+  memset(&S, 0, sizeof(S));
+  S.centroid = -1;
+  EvPair tot, setup;
+  cudaEventCreate(&tot.a); cudaEventCreate(&tot.b);
+  cudaEventCreate(&setup.a); cudaEventCreate(&setup.b);
+  // the store is reset on the run's stream (a fresh DistanceArray)
+  CUDA_TRY(cudaStreamSynchronize(s->st));
+  CUDA_TRY(cudaEventRecord(tot.a, st));
+  CUDA_TRY(cudaEventRecord(setup.a, st));
+  CUDA_TRY(cudaMemsetAsync(s->cnt, 0, (size_t)N * 4, st));
+  CUDA_TRY(launch_store_init(s->mark, NW, s->D, N, st));
+  S.kernels += 1;
+
+  int* d_seq = nullptr;
+  unsigned long long* d_new = nullptr;
+  CUDA_TRY(dalloc(&d_seq, N));
+  CUDA_TRY(dalloc(&d_new, N));
+  CUDA_TRY(cudaMemsetAsync(d_new, 0, (size_t)N * 8, st));
+  int P = 0;
+  int rc = GP_OK;
+
+  if (strategy == GP_STRATEGY_NAIVE && !naive_with_tree) {
+    // naive: the N-1 raster-order sources are independent -> one batch
+    CUDA_TRY(cudaEventRecord(setup.b, st));
+    int rcs = ensure_scratch(c, (size_t)(N - 1));
+    if (rcs) return rcs;
+    std::vector<int32_t> srcs(N - 1);
+    for (int i = 0; i < N - 1; i++) srcs[i] = i;
+    int* d_src = nullptr;
+    CUDA_TRY(dalloc(&d_src, N));
+    CUDA_TRY(cudaMemcpyAsync(d_src, srcs.data(), (N - 1) * 4, cudaMemcpyHostToDevice, st));
+    EvPair pp;
+    cudaEventCreate(&pp.a); cudaEventCreate(&pp.b);
+    CUDA_TRY(cudaEventRecord(pp.a, st));
+    PropArgs a = base_prop(c);
+    a.scratch = c->scratch;
+    a.src = d_src;
+    a.ns = 1;
+    a.D = s->D;
+    a.delta = default_delta(c);
+    CUDA_TRY(launch_propagate(a, N - 1, st));
+    CUDA_TRY(launch_naive_trace(N, NW, s->mark, s->cnt, d_seq, d_new, st));
+    CUDA_TRY(cudaEventRecord(pp.b, st));
+    CUDA_TRY(cudaEventRecord(tot.b, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    S.ms_propagate = ev_ms(pp);
+    S.propagations = N - 1;
+    S.batches = 1;
+    S.kernels += 2;
+    P = N - 1;
+    cudaFree(d_src);
+    cudaEventDestroy(pp.a); cudaEventDestroy(pp.b);
+  } else {
+    // ---- device commit loop with speculative propagation batches ----
+    if (c->tcap < N) {
+      cudaFree(c->tdist);
+      cudaFree(c->tdir);
+      c->tdist = nullptr;
+      c->tdir = nullptr;
+      c->tcap = 0;
+      CUDA_TRY(dalloc(&c->tdist, (size_t)N * N));
+      CUDA_TRY(dalloc(&c->tdir, (size_t)N * N));
+      c->tcap = N;
+    }
+    int *d_slot_of = nullptr, *d_rank = nullptr, *d_ext = nullptr, *d_cands = nullptr;
+    unsigned* d_selkey = nullptr;
+    Ctl* d_ctl = nullptr;
+    float* d_dfc = nullptr;
+    CUDA_TRY(dalloc(&d_slot_of, N));
+    CUDA_TRY(dalloc(&d_rank, N));
+    CUDA_TRY(dalloc(&d_ext, N));
+    CUDA_TRY(dalloc(&d_selkey, N + 2));
+    CUDA_TRY(dalloc(&d_ctl, 1));
+    CUDA_TRY(dalloc(&d_dfc, N));
+    CUDA_TRY(cudaMemsetAsync(d_slot_of, 0xFF, (size_t)N * 4, st));
+    CUDA_TRY(cudaMemsetAsync(d_selkey, 0xFF, (size_t)(N + 2) * 4, st));
+    Ctl h_ctl;
+    memset(&h_ctl, 0, sizeof(h_ctl));
+    h_ctl.cur_src = -1;
+    CUDA_TRY(cudaMemcpyAsync(d_ctl, &h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    if (strategy == GP_STRATEGY_FILLING_RATE) {
+      int cen = -1;
+      std::vector<float> dfc;
+      int r = extrema_device(c, &cen, d_dfc, dfc);
+      if (r) return r;
+      std::vector<int32_t> ext, rank(N);
+      ext_order(dfc, ext);
+      for (int i = 0; i < N; i++) rank[ext[i]] = i;
+      CUDA_TRY(cudaMemcpyAsync(d_rank, rank.data(), N * 4, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(d_ext, ext.data(), N * 4, cudaMemcpyHostToDevice, st));
+      S.centroid = cen;
+      S.propagations += 2;
+      S.kernels += 3;
+    }
+    CUDA_TRY(cudaEventRecord(setup.b, st));
+    int K = spec_k > 0 ? spec_k : 2 * c->nsm;
+    K = std::min(K, N);
+    CUDA_TRY(dalloc(&d_cands, K));
+    int rcs = ensure_scratch(c, (size_t)K);
+    if (rcs) return rcs;
+    CommitArgs ca;
+    memset(&ca, 0, sizeof(ca));
+    ca.g = c->g;
+    ca.strategy = strategy == GP_STRATEGY_FILLING_RATE ? kFillingRate : kNaive;
+    ca.NW = NW;
+    ca.tdist = c->tdist;
+    ca.tdir = c->tdir;
+    ca.slot_of = d_slot_of;
+    ca.mark = s->mark;
+    ca.cnt = s->cnt;
+    ca.D = s->D;
+    ca.rank = d_rank;
+    ca.ext = d_ext;
+    ca.selkey = d_selkey;
+    ca.seq = d_seq;
+    ca.newp = d_new;
+    ca.ctl = d_ctl;
+    ca.max_steps = N + 1;
+    const int nblocks = commit_max_blocks();
+    PropArgs pa = base_prop(c);
+    pa.scratch = c->scratch;
+    pa.src = d_cands;
+    pa.ns = 1;
+    pa.ntrees_dev = &d_ctl->ncand;
+    pa.slot_counter = &d_ctl->nslots;
+    pa.slot_of = d_slot_of;
+    pa.out_dist = c->tdist;
+    pa.out_dir = c->tdir;
+    pa.delta = default_delta(c);
+    std::vector<EvPair> pev, cev;
+    for (int guard = 0; guard < 4 * N + 8; guard++) {
+      EvPair e;
+      cudaEventCreate(&e.a); cudaEventCreate(&e.b);
+      CUDA_TRY(cudaEventRecord(e.a, st));
+      CUDA_TRY(launch_commit(ca, nblocks, st));
+      CUDA_TRY(cudaEventRecord(e.b, st));
+      cev.push_back(e);
+      S.launches++;
+      S.kernels++;
+      CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      if (h_ctl.status == CTL_DONE) break;
+      if (h_ctl.status != CTL_MISS) { rc = fail(GP_EINTERNAL, "commit loop stopped unexpectedly"); break; }
+      if (h_ctl.nslots >= N) { rc = fail(GP_EINTERNAL, "tree store exhausted"); break; }
+      EvPair f;
+      cudaEventCreate(&f.a); cudaEventCreate(&f.b);
+      CUDA_TRY(cudaEventRecord(f.a, st));
+      CUDA_TRY(launch_topk(ca, std::min(K, N - h_ctl.nslots), d_cands, st));
+      CUDA_TRY(launch_propagate(pa, K, st));
+      CUDA_TRY(cudaEventRecord(f.b, st));
+      pev.push_back(f);
+      S.batches++;
+      S.kernels += 2;
+    }
+    CUDA_TRY(cudaEventRecord(tot.b, st));
+    CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (auto& e : cev) { S.ms_commit += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    for (auto& e : pev) { S.ms_propagate += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    P = h_ctl.step;
+    S.propagations += h_ctl.nslots;
+    cudaFree(d_slot_of); cudaFree(d_rank); cudaFree(d_ext); cudaFree(d_cands);
+    cudaFree(d_selkey); cudaFree(d_ctl); cudaFree(d_dfc);
+  }
+  S.ms_total = ev_ms(tot);
+  S.ms_setup = ev_ms(setup);
+  cudaEventDestroy(tot.a); cudaEventDestroy(tot.b);
+  cudaEventDestroy(setup.a); cudaEventDestroy(setup.b);
+  if (rc) { cudaFree(d_seq); cudaFree(d_new); return rc; }
+  std::vector<unsigned long long> nw(P > 0 ? P : 1);
+  if (P > 0) CUDA_TRY(cudaMemcpy(nw.data(), d_new, (size_t)P * 8, cudaMemcpyDeviceToHost));
+  if (seq_out && P > 0) CUDA_TRY(cudaMemcpy(seq_out, d_seq, (size_t)P * 4, cudaMemcpyDeviceToHost));
+  int64_t filled = 0;
+  for (int i = 0; i < P; i++) {
+    filled += (int64_t)nw[i];
+    if (new_out) new_out[i] = (int64_t)nw[i];
+  }
+  cudaFree(d_seq);
+  cudaFree(d_new);
+  s->filled = filled;
+  S.raw_count = P;
+  S.adjusted_count = P + (strategy == GP_STRATEGY_FILLING_RATE ? 2 : 0);
+  S.filled_pairs = filled;
+  if (stats) *stats = S;
+  const int64_t total = ((int64_t)N * N - N) / 2;
+  if (filled != total) return fail(GP_EINTERNAL, "run ended with " + std::to_string(filled) +
+                                                     " of " + std::to_string(total) + " pairs");
+  return GP_OK;
+}

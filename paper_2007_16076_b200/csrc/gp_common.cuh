@@ -1,0 +1,57 @@
+// Shared device helpers for the geopairs B200 kernels.
+//
+// Pixel graph: H x W image, row-major pixel ids, 8- or 4-connectivity.
+// Neighbour positions are encoded by their index k in the 3x3 window
+// (k = (dr+1)*3 + (dc+1), k != 4), visited in ascending k == ascending
+// neighbour id, the order of the reference's lexsorted CSR
+// (propagation.py:13,85).  A tree's parent link is stored as that code
+// (one byte per pixel, GP_ROOT for roots): parent(v) = v + (k/3-1)*W + (k%3-1).
+//
+// Arithmetic: every distance is fp32.  Integer images (grey levels 1..255)
+// stay exact: weights are integers <= 1020 and every geodesic distance of a
+// <= 4096 x 4096 image stays below 2^24, so fp32 sums are exact and equal the
+// reference's int64 values (checked on the host before a run).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gp {
+
+enum Metric : int { kL1 = 0, kSum = 1, kMean = 2 };
+enum Strategy : int { kNaive = 0, kFillingRate = 1 };
+
+constexpr uint8_t GP_ROOT = 0xFF;
+constexpr uint32_t INF_BITS = 0x7F800000u;  // +inf; non-negative floats order as uint32
+constexpr unsigned long long KEY_NONE = ~0ull;
+
+struct Grid {
+  int H, W, N, conn, metric;
+};
+
+// scaled_weight (grid.py:146-154) in fp32, no contraction: SUM = 2*fl(a+b).
+__device__ __forceinline__ float edge_w(int metric, float a, float b) {
+  if (metric == kSum) return __fmul_rn(2.0f, __fadd_rn(a, b));
+  if (metric == kMean) return __fadd_rn(a, b);
+  return __fmul_rn(2.0f, fabsf(__fsub_rn(a, b)));
+}
+
+// Is window position k a neighbour under this connectivity?
+__device__ __forceinline__ bool k_in_conn(int conn, int k) {
+  return k != 4 && (conn == 8 || (k & 1));
+}
+
+// Neighbour of pixel (r, c) at window position k, or -1 if off-image.
+__device__ __forceinline__ int nbr_at(const Grid& g, int r, int c, int k) {
+  int rr = r + k / 3 - 1, cc = c + k % 3 - 1;
+  if (rr < 0 || rr >= g.H || cc < 0 || cc >= g.W) return -1;
+  return rr * g.W + cc;
+}
+
+__device__ __forceinline__ int parent_of(int v, uint8_t code, int W) {
+  return code == GP_ROOT ? -1 : v + (code / 3 - 1) * W + (code % 3 - 1);
+}
+
+__device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ int ldcg_i32(const int* p) { return __ldcg(p); }
+
+}  // namespace gp

@@ -1,0 +1,158 @@
+"""Generate the committed golden fixtures under tests/golden/.
+
+Run in the build container (NOT on the GPU box -- /root/reference does not
+exist there):
+
+    python tests/golden/make_golden.py small      # reference, tiny images
+    python tests/golden/make_golden.py cfg 2      # reference itself (int config)
+    python tests/golden/make_golden.py cfg 4      # reference itself, force=True
+    python tests/golden/make_golden.py cfg 1|3|5  # fp32 restatement (oracle/)
+
+Integer configs (2, 4) and every ``small`` case come from the UNMODIFIED
+reference package imported from /root/reference/pkg/src.  The reference
+rejects fp32 images and 4-connectivity (grid.py:49-57, propagation.py:13), so
+configs 1, 3 and 5 come from the fp32 restatement in oracle/, whose integer
+mode is pinned bit-for-bit to the reference by the ``small`` fixtures and
+configs 2/4 (tests/test_oracle.py).
+
+Fixture contents per config (kept small enough to commit):
+  seq, new (pairs per commit), raw, adjusted, centroid, visits (oracle only),
+  d_sha256 (sha256 of D as little-endian int32 for int configs / float32),
+  row_sum (float64 per-row sums of D), samp_i/samp_j/samp_v (random entries),
+  tree_src/tree_dist/tree_parent (propagations of the first committed sources).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from paper_2007_16076_b200.configs import CONFIGS, make_image  # noqa: E402
+
+N_SAMPLES = 100_000
+N_TREES = 4
+
+
+def d_digest(D: np.ndarray, isf: bool) -> str:
+    arr = D.astype("<f4" if isf else "<i4")
+    return hashlib.sha256(arr.tobytes()).hexdigest()
+
+
+def _samples(D: np.ndarray, seed: int):
+    n = D.shape[0]
+    rng = np.random.default_rng(seed)
+    i = rng.integers(0, n, N_SAMPLES)
+    j = rng.integers(0, n, N_SAMPLES)
+    return i.astype(np.int32), j.astype(np.int32), D[i, j]
+
+
+def _ref():
+    sys.path.insert(0, "/root/reference/pkg/src")
+    import geopairs  # noqa: F401
+
+    return geopairs
+
+
+def make_small():
+    gp = _ref()
+    rng = np.random.default_rng(2007)
+    out = {}
+    cases = 0
+    metrics = [gp.Metric.SUM, gp.Metric.MEAN, gp.Metric.L1]
+    for t in range(48):
+        h, w = (int(x) for x in rng.integers(1, 11, 2))
+        if h * w < 2:
+            continue
+        img = rng.integers(1, 256, (h, w))
+        if t % 4 == 1:  # tie-heavy images: few grey levels
+            img = rng.integers(1, 4, (h, w))
+        metric = metrics[t % 3] if t % 4 != 3 else gp.Metric.SUM
+        image = gp.Image(img)
+        graph = gp.GridGraph(image, metric)
+        n = h * w
+        dist = np.stack([graph.propagate([s]).dist for s in range(n)])
+        parent = np.stack([graph.propagate([s]).parent for s in range(n)])
+        k = f"c{cases}_"
+        out[k + "img"] = img.astype(np.int64)
+        out[k + "metric"] = np.array(metric.value)
+        out[k + "dist"] = dist
+        out[k + "parent"] = parent
+        ctx = gp.compute_extrema_context(image, metric)
+        out[k + "centroid"] = np.array(ctx.centroid)
+        out[k + "dfc"] = ctx.dist_from_c
+        out[k + "ext"] = ctx.ext
+        for kind in (gp.StrategyKind.NAIVE, gp.StrategyKind.FILLING_RATE):
+            run = gp.run_strategy(image, metric, kind)
+            tag = "naive" if kind is gp.StrategyKind.NAIVE else "fr"
+            out[k + tag + "_D"] = run.distances.dist
+            out[k + tag + "_seq"] = np.array([s for _, s, _ in run.trace.samples], dtype=np.int64)
+            out[k + tag + "_adj"] = np.array(run.trace.adjusted_count)
+            out[k + tag + "_counts"] = np.array(run.distances.point_filled_counts)
+        cases += 1
+    out["n_cases"] = np.array(cases)
+    np.savez_compressed(os.path.join(HERE, "ref_small.npz"), **out)
+    print("small cases:", cases)
+
+
+def make_cfg(index: int, nthreads: int):
+    spec = CONFIGS[index]
+    img = make_image(index)
+    isf = spec.dtype == "f32"
+    t0 = time.time()
+    if not isf:
+        gp = _ref()
+        image = gp.Image(img.astype(np.int64))
+        kind = gp.StrategyKind.FILLING_RATE if spec.strategy == "filling-rate" else gp.StrategyKind.NAIVE
+        run = gp.run_strategy(image, gp.Metric.SUM, kind, force=True)
+        D = run.distances.dist
+        seq = np.array([s for _, s, _ in run.trace.samples], dtype=np.int64)
+        A = spec.total_pairs
+        filled = np.array([int(tau * A) for _, _, tau in run.trace.samples], dtype=np.int64)
+        new = np.diff(np.concatenate([[0], filled]))
+        raw, adjusted = run.trace.raw_count, run.trace.adjusted_count
+        centroid = gp.compute_extrema_context(image, gp.Metric.SUM).centroid if spec.strategy != "naive" else -1
+        graph = gp.GridGraph(image, gp.Metric.SUM)
+        trees = [graph.propagate([int(s)]) for s in seq[:N_TREES]]
+        tree_dist = np.stack([t.dist for t in trees])
+        tree_parent = np.stack([t.parent for t in trees])
+        visits = np.zeros(0, dtype=np.int64)
+        source = "reference geopairs (run_strategy, force=True)"
+    else:
+        sys.path.insert(0, ROOT)
+        from oracle import oracle as O
+
+        r = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads)
+        D, seq, new, raw, adjusted, centroid = r["D"], r["seq"], r["new"], r["raw"], r["adjusted"], r["centroid"]
+        visits = r["visits"]
+        trees = [O.propagate(img, [int(s)], conn=spec.conn) for s in seq[:N_TREES]]
+        tree_dist = np.stack([t[0] for t in trees])
+        tree_parent = np.stack([t[1] for t in trees])
+        source = "fp32 restatement (oracle/oracle.c)"
+    elapsed = time.time() - t0
+    si, sj, sv = _samples(D, 1000 + index)
+    out = dict(
+        seq=seq.astype(np.int32), new=new.astype(np.int64), raw=np.array(raw),
+        adjusted=np.array(adjusted), centroid=np.array(centroid), visits=visits,
+        d_sha256=np.array(d_digest(D, isf)), row_sum=D.astype(np.float64).sum(axis=1),
+        samp_i=si, samp_j=sj, samp_v=sv, tree_src=seq[:N_TREES].astype(np.int32),
+        tree_dist=tree_dist, tree_parent=tree_parent.astype(np.int32),
+        source=np.array(source), cpu_seconds=np.array(elapsed),
+        cpu_threads=np.array(1 if not isf else nthreads),
+    )
+    np.savez_compressed(os.path.join(HERE, f"cfg{index}.npz"), **out)
+    print(f"cfg{index}: raw={raw} adjusted={adjusted} elapsed={elapsed:.1f}s src={source}")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "small":
+        make_small()
+    else:
+        make_cfg(int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 8)
