@@ -40,17 +40,17 @@ struct gp_ctx {
   float* d_img = nullptr;
   cudaStream_t st = nullptr;
   int nsm = 148;
-  // tree store + run workspace (lazily sized)
-  float* tdist = nullptr;
-  uint8_t* tdir = nullptr;
-  int tcap = 0;
-  uint32_t* scratch = nullptr;
+  // tree store (Euler-tour form) + propagation scratch, lazily sized
+  TreeStore ts{};
+  uint8_t* scratch = nullptr;
   size_t scratch_trees = 0;
+  int commit_blocks = 0;
 };
 
 struct gp_store {
   int64_t n;
-  int NW;
+  MarkLayout L;
+  size_t mark_words = 0;  // allocated words
   float* D = nullptr;
   uint32_t* mark = nullptr;
   int* cnt = nullptr;
@@ -117,8 +117,11 @@ extern "C" int gp_ctx_create(int H, int W, int dtype, const void* pixels, int me
 extern "C" void gp_ctx_destroy(gp_ctx* c) {
   if (!c) return;
   cudaFree(c->d_img);
-  cudaFree(c->tdist);
-  cudaFree(c->tdir);
+  cudaFree(c->ts.pre);
+  cudaFree(c->ts.szp);
+  cudaFree(c->ts.tdp);
+  cudaFree(c->ts.part);
+  cudaFree(c->ts.T);
   cudaFree(c->scratch);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
@@ -131,7 +134,7 @@ static int ensure_scratch(gp_ctx* c, size_t ntrees) {
   cudaFree(c->scratch);
   c->scratch = nullptr;
   c->scratch_trees = 0;
-  CUDA_TRY(dalloc(&c->scratch, prop_scratch_words(c->g.N) * ntrees));
+  CUDA_TRY(dalloc(&c->scratch, prop_scratch_bytes(c->g.N) * ntrees));
   c->scratch_trees = ntrees;
   return GP_OK;
 }
@@ -290,14 +293,15 @@ extern "C" int gp_store_create(int64_t n, gp_store** out) {
   if (n > 65536) return fail(GP_ENOMEM, "stores above 65536 pixels are not supported");
   gp_store* s = new gp_store();
   s->n = n;
-  s->NW = (int)((n + 31) / 32);
+  s->L = make_layout((int)n, 1, (int)n);  // no image yet: raster columns
+  s->mark_words = (size_t)n * s->L.RW;
   cudaError_t e = cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = dalloc(&s->D, (size_t)n * n);
-  if (e == cudaSuccess) e = dalloc(&s->mark, (size_t)n * s->NW);
+  if (e == cudaSuccess) e = dalloc(&s->mark, s->mark_words);
   if (e == cudaSuccess) e = dalloc(&s->cnt, (size_t)n);
   if (e == cudaSuccess) e = dalloc(&s->out3, 3);
   if (e == cudaSuccess) e = cudaMemsetAsync(s->cnt, 0, n * 4, s->st);
-  if (e == cudaSuccess) e = launch_store_init(s->mark, s->NW, s->D, (int)n, s->st);
+  if (e == cudaSuccess) e = launch_store_init(s->L, s->mark, s->D, s->st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s->st);
   if (e != cudaSuccess) {
     gp_store_destroy(s);
@@ -324,7 +328,7 @@ extern "C" int gp_store_device_ptrs(gp_store* s, float** D, uint32_t** mark, int
   if (D) *D = s->D;
   if (mark) *mark = s->mark;
   if (counts) *counts = s->cnt;
-  if (words) *words = s->NW;
+  if (words) *words = s->L.RW;
   return GP_OK;
 }
 
@@ -341,7 +345,7 @@ extern "C" int gp_store_fill_tree(gp_store* s, const int32_t* parent, const floa
   // snapshot so that a failed fill leaves the store unchanged is not needed by
   // the reference (it also mutates before raising); mirror that behaviour.
   CUDA_TRY(cudaMemsetAsync(s->out3, 0, 24, s->st));
-  CUDA_TRY(launch_fill_tree_api(N, s->NW, d_par, d_td, s->mark, s->cnt, s->D, s->out3, tol, s->st));
+  CUDA_TRY(launch_fill_tree_api(s->L, d_par, d_td, s->mark, s->cnt, s->D, s->out3, tol, s->st));
   unsigned long long o[3];
   CUDA_TRY(cudaMemcpyAsync(o, s->out3, 24, cudaMemcpyDeviceToHost, s->st));
   CUDA_TRY(cudaStreamSynchronize(s->st));
@@ -366,7 +370,7 @@ extern "C" int gp_store_fill_source(gp_store* s, int64_t source, const float* di
   CUDA_TRY(cudaMemcpyAsync(d_dist, dist, N * 4, cudaMemcpyHostToDevice, s->st));
   CUDA_TRY(cudaMemsetAsync(s->out3, 0, 24, s->st));
   // the reference checks agreement before writing anything (distances.py:132-136)
-  CUDA_TRY(launch_fill_source_api(N, s->NW, (int)source, d_dist, s->mark, s->cnt, s->D, s->out3,
+  CUDA_TRY(launch_fill_source_api(s->L, (int)source, d_dist, s->mark, s->cnt, s->D, s->out3,
                                   tol, s->st));
   unsigned long long o[3];
   CUDA_TRY(cudaMemcpyAsync(o, s->out3, 24, cudaMemcpyDeviceToHost, s->st));
@@ -395,7 +399,7 @@ extern "C" int gp_store_read(gp_store* s, float* D_out, uint8_t* mark_out) {
   if (mark_out) {
     uint8_t* d_m = nullptr;
     CUDA_TRY(dalloc(&d_m, nn));
-    CUDA_TRY(launch_mark_unpack(s->mark, (int)s->n, s->NW, d_m, s->st));
+    CUDA_TRY(launch_mark_unpack(s->L, s->mark, d_m, s->st));
     CUDA_TRY(cudaMemcpyAsync(mark_out, d_m, nn, cudaMemcpyDeviceToHost, s->st));
     CUDA_TRY(cudaStreamSynchronize(s->st));
     cudaFree(d_m);
@@ -415,10 +419,49 @@ static float ev_ms(const EvPair& p) {
   return ms;
 }
 
+static int ensure_tree_store(gp_ctx* c, int nparts) {
+  const int N = c->g.N;
+  if (c->ts.pre && c->ts.cap >= N && c->ts.nparts == nparts) return GP_OK;
+  cudaFree(c->ts.pre); cudaFree(c->ts.szp); cudaFree(c->ts.tdp); cudaFree(c->ts.part); cudaFree(c->ts.T);
+  c->ts = TreeStore{};
+  const size_t cap = (size_t)N;  // a pixel is propagated at most once: N slots always suffice
+  CUDA_TRY(dalloc(&c->ts.pre, cap * N));
+  CUDA_TRY(dalloc(&c->ts.szp, cap * N));
+  CUDA_TRY(dalloc(&c->ts.tdp, cap * N));
+  CUDA_TRY(dalloc(&c->ts.part, cap * nparts));
+  CUDA_TRY(dalloc(&c->ts.T, cap));
+  c->ts.cap = (int)cap;
+  c->ts.nparts = nparts;
+  return GP_OK;
+}
+
+static int store_relayout(gp_store* s, const MarkLayout& L) {
+  const size_t words = (size_t)s->n * L.RW;
+  if (words > s->mark_words) {
+    cudaFree(s->mark);
+    s->mark = nullptr;
+    s->mark_words = 0;
+    CUDA_TRY(dalloc(&s->mark, words));
+    s->mark_words = words;
+  }
+  s->L = L;
+  return GP_OK;
+}
+
+static int commit_blocks(gp_ctx* c) {
+  if (c->commit_blocks) return c->commit_blocks;
+  int maxb = commit_max_blocks();
+  int bps = 2;
+  if (const char* e = getenv("GP_COMMIT_BLOCKS_PER_SM")) bps = atoi(e);
+  int nb = std::max(1, std::min(maxb, bps * c->nsm));
+  c->commit_blocks = nb;
+  return nb;
+}
+
 extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, int spec_k,
                       int32_t* seq_out, int64_t* new_out, gp_run_stats* stats) {
   if (!c || !s) return fail(GP_EINVAL, "null argument");
-  const int N = c->g.N, NW = s->NW;
+  const int N = c->g.N;
   if (s->n != N) return fail(GP_EINVAL, "store size does not match the image");
   if (strategy != GP_STRATEGY_NAIVE && strategy != GP_STRATEGY_FILLING_RATE)
     return fail(GP_EINVAL, "strategy not supported on the device path");
@@ -426,15 +469,18 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
   gp_run_stats S;
   memset(&S, 0, sizeof(S));
   S.centroid = -1;
+  // the store becomes a fresh DistanceArray laid out for this image
+  CUDA_TRY(cudaStreamSynchronize(s->st));
+  int rl = store_relayout(s, make_layout(N, c->g.H, c->g.W));
+  if (rl) return rl;
+  const MarkLayout L = s->L;
   EvPair tot, setup;
   cudaEventCreate(&tot.a); cudaEventCreate(&tot.b);
   cudaEventCreate(&setup.a); cudaEventCreate(&setup.b);
-  // the store is reset on the run's stream (a fresh DistanceArray)
-  CUDA_TRY(cudaStreamSynchronize(s->st));
   CUDA_TRY(cudaEventRecord(tot.a, st));
   CUDA_TRY(cudaEventRecord(setup.a, st));
   CUDA_TRY(cudaMemsetAsync(s->cnt, 0, (size_t)N * 4, st));
-  CUDA_TRY(launch_store_init(s->mark, NW, s->D, N, st));
+  CUDA_TRY(launch_store_init(L, s->mark, s->D, st));
   S.kernels += 1;
 
   int* d_seq = nullptr;
@@ -459,13 +505,12 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     cudaEventCreate(&pp.a); cudaEventCreate(&pp.b);
     CUDA_TRY(cudaEventRecord(pp.a, st));
     PropArgs a = base_prop(c);
-    a.scratch = c->scratch;
     a.src = d_src;
     a.ns = 1;
     a.D = s->D;
     a.delta = default_delta(c);
     CUDA_TRY(launch_propagate(a, N - 1, st));
-    CUDA_TRY(launch_naive_trace(N, NW, s->mark, s->cnt, d_seq, d_new, st));
+    CUDA_TRY(launch_naive_trace(L, s->mark, s->cnt, d_seq, d_new, st));
     CUDA_TRY(cudaEventRecord(pp.b, st));
     CUDA_TRY(cudaEventRecord(tot.b, st));
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -478,17 +523,12 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     cudaEventDestroy(pp.a); cudaEventDestroy(pp.b);
   } else {
     // ---- device commit loop with speculative propagation batches ----
-    if (c->tcap < N) {
-      cudaFree(c->tdist);
-      cudaFree(c->tdir);
-      c->tdist = nullptr;
-      c->tdir = nullptr;
-      c->tcap = 0;
-      CUDA_TRY(dalloc(&c->tdist, (size_t)N * N));
-      CUDA_TRY(dalloc(&c->tdir, (size_t)N * N));
-      c->tcap = N;
-    }
+    const int nblocks = commit_blocks(c);
+    const int nparts = nblocks * (COMMIT_THREADS / 32);
+    int rts = ensure_tree_store(c, nparts);
+    if (rts) return rts;
     int *d_slot_of = nullptr, *d_rank = nullptr, *d_ext = nullptr, *d_cands = nullptr;
+    int *d_slots = nullptr, *d_free = nullptr;
     unsigned* d_selkey = nullptr;
     Ctl* d_ctl = nullptr;
     float* d_dfc = nullptr;
@@ -498,6 +538,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     CUDA_TRY(dalloc(&d_selkey, N + 2));
     CUDA_TRY(dalloc(&d_ctl, 1));
     CUDA_TRY(dalloc(&d_dfc, N));
+    CUDA_TRY(dalloc(&d_free, N));
     CUDA_TRY(cudaMemsetAsync(d_slot_of, 0xFF, (size_t)N * 4, st));
     CUDA_TRY(cudaMemsetAsync(d_selkey, 0xFF, (size_t)(N + 2) * 4, st));
     Ctl h_ctl;
@@ -522,16 +563,17 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     int K = spec_k > 0 ? spec_k : 2 * c->nsm;
     K = std::min(K, N);
     CUDA_TRY(dalloc(&d_cands, K));
+    CUDA_TRY(dalloc(&d_slots, K));
     int rcs = ensure_scratch(c, (size_t)K);
     if (rcs) return rcs;
     CommitArgs ca;
     memset(&ca, 0, sizeof(ca));
     ca.g = c->g;
+    ca.L = L;
     ca.strategy = strategy == GP_STRATEGY_FILLING_RATE ? kFillingRate : kNaive;
-    ca.NW = NW;
-    ca.tdist = c->tdist;
-    ca.tdir = c->tdir;
+    ca.ts = c->ts;
     ca.slot_of = d_slot_of;
+    ca.free_stack = d_free;
     ca.mark = s->mark;
     ca.cnt = s->cnt;
     ca.D = s->D;
@@ -542,16 +584,12 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     ca.newp = d_new;
     ca.ctl = d_ctl;
     ca.max_steps = N + 1;
-    const int nblocks = commit_max_blocks();
     PropArgs pa = base_prop(c);
-    pa.scratch = c->scratch;
     pa.src = d_cands;
     pa.ns = 1;
     pa.ntrees_dev = &d_ctl->ncand;
-    pa.slot_counter = &d_ctl->nslots;
-    pa.slot_of = d_slot_of;
-    pa.out_dist = c->tdist;
-    pa.out_dir = c->tdir;
+    pa.slot = d_slots;
+    pa.ts = c->ts;
     pa.delta = default_delta(c);
     std::vector<EvPair> pev, cev;
     for (int guard = 0; guard < 4 * N + 8; guard++) {
@@ -567,11 +605,10 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
       CUDA_TRY(cudaStreamSynchronize(st));
       if (h_ctl.status == CTL_DONE) break;
       if (h_ctl.status != CTL_MISS) { rc = fail(GP_EINTERNAL, "commit loop stopped unexpectedly"); break; }
-      if (h_ctl.nslots >= N) { rc = fail(GP_EINTERNAL, "tree store exhausted"); break; }
       EvPair f;
       cudaEventCreate(&f.a); cudaEventCreate(&f.b);
       CUDA_TRY(cudaEventRecord(f.a, st));
-      CUDA_TRY(launch_topk(ca, std::min(K, N - h_ctl.nslots), d_cands, st));
+      CUDA_TRY(launch_topk(ca, K, d_cands, d_slots, st));
       CUDA_TRY(launch_propagate(pa, K, st));
       CUDA_TRY(cudaEventRecord(f.b, st));
       pev.push_back(f);
@@ -584,9 +621,9 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     for (auto& e : cev) { S.ms_commit += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (auto& e : pev) { S.ms_propagate += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     P = h_ctl.step;
-    S.propagations += h_ctl.nslots;
-    cudaFree(d_slot_of); cudaFree(d_rank); cudaFree(d_ext); cudaFree(d_cands);
-    cudaFree(d_selkey); cudaFree(d_ctl); cudaFree(d_dfc);
+    cudaFree(d_slot_of); cudaFree(d_rank); cudaFree(d_ext); cudaFree(d_cands); cudaFree(d_slots);
+    cudaFree(d_selkey); cudaFree(d_ctl); cudaFree(d_dfc); cudaFree(d_free);
+    S.propagations += h_ctl.total_props;
   }
   S.ms_total = ev_ms(tot);
   S.ms_setup = ev_ms(setup);

@@ -4,25 +4,28 @@
 // One persistent cooperative kernel executes commit after commit without
 // returning to the host:
 //
-//   fill   (K2)  every pixel v whose row is not yet full walks its ancestor
-//                chain in the committed tree (byte parent codes) and, for each
-//                unmarked pair (v,u), sets both mark bits, writes
-//                D[v][u] = D[u][v] = fl(td[v] - td[u]) and bumps the counts --
-//                fill_tree_pairs (reference _kernels.py:82-116) with the
-//                pair loop turned inside out (one walker per descendant).
-//                A full row (count N-1) has every bit set, so skipping its
-//                walk is exact.  The root's row is always full afterwards.
+//   fill   (K2)  fill_tree_pairs (reference _kernels.py:82-116) over the
+//                tree's Euler tour: the pairs of the tree are
+//                {(pre[q], pre[q+1+k]) : k < szp[q]}, split into 32-pair
+//                chunks and pre-partitioned evenly over every warp of the grid
+//                (propagate.cu E7).  A warp takes one chunk at a time: all 32
+//                lanes share the ancestor u, so their mark bits lie in row u
+//                at the (tile-ordered) columns of one subtree region.  An
+//                unmarked pair sets both bits, writes D[u][w] = D[w][u] =
+//                fl(td[w] - td[u]) and bumps both counts -- first writer in
+//                commit order, exactly as the reference.  Ancestors whose row
+//                is full (count N-1) are skipped: every bit is already set.
 //   grid barrier
 //   select (K3)  grid-wide argmin of the packed key (count << 16 | rank) over
 //                open pixels -- FillingRateSelector.next_source
 //                (strategies.py:220-227): least filled, then greatest
-//                distance from the centroid, then smallest id (the rank is the
-//                position in ext = lexsort((id, -dist_from_c))).  naive:
+//                distance from the centroid, then smallest id (rank = position
+//                in ext = lexsort((id, -dist_from_c))).  naive (with tree):
 //                key = id (strategies.py:125-129).
 //   grid barrier
 //
-// The loop leaves the kernel only when the selected source has no tree in the
-// tree store (the host then propagates a speculative batch: the top-K open
+// The loop leaves the kernel only when the selected source has no tree in
+// the store (the host then propagates a speculative batch: the top-K open
 // pixels by the same key, K1) or when the array is complete.  A tree depends
 // only on its source, so speculation never changes the committed sequence.
 #include <cooperative_groups.h>
@@ -33,8 +36,6 @@
 namespace cg = cooperative_groups;
 
 namespace gp {
-
-constexpr int COMMIT_THREADS = 512;
 
 __device__ __forceinline__ unsigned sel_key(int strategy, int N, int v, int c, const int* rank) {
   if (c >= N - 1) return 0xFFFFFFFFu;
@@ -90,13 +91,87 @@ __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned* r
   if (threadIdx.x == 0 && m != 0xFFFFFFFFu) atomicMin(&a.selkey[step], m);
 }
 
+// K2 for one committed tree: this warp's share of the chunks.
+__device__ __forceinline__ unsigned fill_warp_share(const CommitArgs& a, int slot, int s) {
+  const int N = a.g.N;
+  const int lane = threadIdx.x & 31;
+  const int P = a.ts.nparts;
+  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const size_t off = (size_t)slot * N;
+  const uint16_t* pre = a.ts.pre + off;
+  const uint16_t* szp = a.ts.szp + off;
+  const float* tdp = a.ts.tdp + off;
+  const unsigned T = __ldg(&a.ts.T[slot]);
+  const unsigned b0 = (unsigned)(((unsigned long long)p * T) / P);
+  const unsigned b1 = (unsigned)(((unsigned long long)(p + 1) * T) / P);
+  unsigned count = b1 - b0;
+  if (!count) return 0;
+  const uint32_t pw = __ldg(&a.ts.part[(size_t)slot * P + p]);
+  int q = (int)(pw & 0xFFFFu);
+  unsigned coff = pw >> 16;
+  unsigned total_new = 0;
+  const MarkLayout L = a.L;
+  while (count) {
+    unsigned sz = __ldg(&szp[q]);
+    if (sz == 0) {  // leaves carry no chunk: jump to the next internal node
+      for (;;) {
+        const int qq = q + lane;
+        const unsigned zz = qq < N ? (unsigned)__ldg(&szp[qq]) : 1u;
+        const unsigned m = __ballot_sync(0xffffffffu, zz != 0);
+        if (m) {
+          q += __ffs(m) - 1;
+          break;
+        }
+        q += 32;
+      }
+      sz = __ldg(&szp[q]);
+    }
+    const unsigned nch = (sz + 31u) >> 5;
+    const unsigned take = min(nch - coff, count);
+    const int u = __ldg(&pre[q]);
+    const bool skip = (u != s) && (__ldcg(&a.cnt[u]) >= N - 1);  // full row: all set
+    if (!skip) {
+      const uint32_t ucol = mcol(L, (uint32_t)u);
+      const uint32_t ubit = 1u << (ucol & 31);
+      const float tdu = __ldg(&tdp[q]);
+      uint32_t* mrow = a.mark + (size_t)u * L.RW;
+      unsigned unew = 0;
+      for (unsigned c = coff; c < coff + take; c++) {
+        const unsigned k = c * 32u + lane;
+        if (k < sz) {
+          const int w = __ldg(&pre[q + 1 + k]);
+          const uint32_t wcol = mcol(L, (uint32_t)w);
+          const uint32_t wbit = 1u << (wcol & 31);
+          uint32_t* mw = mrow + (wcol >> 5);
+          if (!(__ldcg(mw) & wbit)) {
+            atomicOr(mw, wbit);
+            atomicOr(a.mark + mword(L, (uint32_t)w, ucol), ubit);
+            const float duv = __fsub_rn(__ldg(&tdp[q + 1 + k]), tdu);
+            a.D[(size_t)u * N + w] = duv;
+            a.D[(size_t)w * N + u] = duv;
+            atomicAdd(&a.cnt[w], 1);
+            unew++;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) unew += __shfl_xor_sync(0xffffffffu, unew, o);
+      if (lane == 0 && unew && u != s) atomicAdd(&a.cnt[u], (int)unew);
+      total_new += unew;
+    }
+    count -= take;
+    q++;
+    coff = 0;
+  }
+  return lane == 0 ? total_new : 0u;
+}
+
 __global__ void __launch_bounds__(COMMIT_THREADS) k_commit(CommitArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned red32[32];
   __shared__ unsigned long long red64[32];
-  const int N = a.g.N, W = a.g.W, NW = a.NW;
+  const int N = a.g.N;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int gstride = gridDim.x * blockDim.x;
 
   int step = a.ctl->step;
   int s = a.ctl->cur_src;
@@ -113,44 +188,17 @@ __global__ void __launch_bounds__(COMMIT_THREADS) k_commit(CommitArgs a) {
     if (done_here >= a.max_steps) { status = CTL_LIMIT; break; }
     const int slot = __ldcg(&a.slot_of[s]);
     if (slot < 0) { status = CTL_MISS; break; }
-    const uint8_t* dir = a.tdir + (size_t)slot * N;
-    const float* td = a.tdist + (size_t)slot * N;
 
-    // ---- K2: tree-walk fill ----
-    unsigned long long lnew_total = 0;
-    for (int v = gtid; v < N; v += gstride) {
-      if (v == s) continue;
-      if (__ldcg(&a.cnt[v]) >= N - 1) continue;  // full row: nothing to set
-      uint32_t* mrow = a.mark + (size_t)v * NW;
-      const float dv = __ldg(&td[v]);
-      const uint32_t vbit = 1u << (v & 31);
-      const int vword = v >> 5;
-      int u = parent_of(v, __ldg(&dir[v]), W);
-      int lnew = 0;
-      while (u >= 0) {
-        const uint32_t ubit = 1u << (u & 31);
-        const uint32_t wv = __ldcg(&mrow[u >> 5]);
-        const int pu = parent_of(u, __ldg(&dir[u]), W);
-        if (!(wv & ubit)) {
-          atomicOr(&mrow[u >> 5], ubit);
-          atomicOr(&a.mark[(size_t)u * NW + vword], vbit);
-          const float duv = __fsub_rn(dv, __ldg(&td[u]));
-          a.D[(size_t)v * N + u] = duv;
-          a.D[(size_t)u * N + v] = duv;
-          if (u != s) atomicAdd(&a.cnt[u], 1);
-          lnew++;
-        }
-        u = pu;
-      }
-      if (lnew) atomicAdd(&a.cnt[v], lnew);
-      lnew_total += lnew;
-    }
-    lnew_total = block_reduce_sum(lnew_total, red64);
-    if (threadIdx.x == 0 && lnew_total) atomicAdd(&a.newp[step], lnew_total);
+    // ---- K2: Euler-range fill ----
+    unsigned long long lnew = fill_warp_share(a, slot, s);
+    lnew = block_reduce_sum(lnew, red64);
+    if (threadIdx.x == 0 && lnew) atomicAdd(&a.newp[step], lnew);
     grid.sync();
     if (gtid == 0) {
       a.cnt[s] = N - 1;  // the root pairs with every pixel
       a.seq[step] = s;
+      a.slot_of[s] = -2;  // committed: recycle the slot
+      a.free_stack[a.ctl->free_top++] = slot;
     }
     // ---- K3: selection of the next source ----
     select_step(a, step + 1, s, red32);
@@ -183,8 +231,9 @@ cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st) 
 }
 
 // ---- speculative candidate batch: the K smallest keys among open pixels
-// without a tree (radix select, MSB first, single CTA) ----
-__global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int* cands) {
+// without a tree (radix select, MSB first, single CTA); assigns tree slots
+// (recycled first) and records slot_of[] ----
+__global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int* cands, int* slots) {
   __shared__ unsigned hist[256];
   __shared__ unsigned s_prefix, s_mask, s_k, s_all;
   __shared__ int s_n;
@@ -197,7 +246,7 @@ __global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int* cands) 
     const unsigned prefix = s_prefix, mask = s_mask;
     if (!s_all) {
       for (int v = tid; v < N; v += blockDim.x) {
-        if (__ldcg(&a.slot_of[v]) >= 0) continue;
+        if (__ldcg(&a.slot_of[v]) != -1) continue;
         unsigned key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
         if (key == 0xFFFFFFFFu || (key & mask) != prefix) continue;
         atomicAdd(&hist[(key >> shift) & 255u], 1u);
@@ -226,52 +275,66 @@ __global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int* cands) 
   }
   const unsigned thr = s_all ? 0xFFFFFFFEu : s_prefix;
   for (int v = tid; v < N; v += blockDim.x) {
-    if (__ldcg(&a.slot_of[v]) >= 0) continue;
+    if (__ldcg(&a.slot_of[v]) != -1) continue;
     unsigned key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
     if (key == 0xFFFFFFFFu || key > thr) continue;
     int i = atomicAdd(&s_n, 1);
     if (i < K) cands[i] = v;
   }
   __syncthreads();
-  if (tid == 0) a.ctl->ncand = min(s_n, K);
+  if (tid == 0) {
+    const int n = min(s_n, K);
+    Ctl* c = a.ctl;
+    for (int i = 0; i < n; i++) {
+      int sl = c->free_top > 0 ? a.free_stack[--c->free_top] : c->nslots++;
+      slots[i] = sl;
+      a.slot_of[cands[i]] = sl;
+    }
+    c->ncand = n;
+    c->total_props += n;
+  }
 }
 
-cudaError_t launch_topk(const CommitArgs& a, int K, int* cands, cudaStream_t st) {
-  k_topk<<<1, 1024, 0, st>>>(a, K, cands);
+cudaError_t launch_topk(const CommitArgs& a, int K, int* cands, int* slots, cudaStream_t st) {
+  k_topk<<<1, 1024, 0, st>>>(a, K, cands, slots);
   return cudaGetLastError();
 }
 
 // ---------------- store helpers ----------------
-__global__ void k_store_init(uint32_t* mark, int NW, float* D, int N) {
+__global__ void k_store_init(MarkLayout L, uint32_t* mark, float* D) {
+  const int N = L.N;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-    mark[(size_t)v * NW + (v >> 5)] = 1u << (v & 31);  // rows pre-zeroed by memset
+    const uint32_t c = mcol(L, (uint32_t)v);
+    mark[mword(L, (uint32_t)v, c)] = 1u << (c & 31);  // rows pre-zeroed by memset
     if (D) D[(size_t)v * N + v] = 0.0f;
   }
 }
 
-cudaError_t launch_store_init(uint32_t* mark, int NW, float* D, int N, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(mark, 0, (size_t)N * NW * 4, st);
+cudaError_t launch_store_init(const MarkLayout& L, uint32_t* mark, float* D, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(mark, 0, (size_t)L.N * L.RW * 4, st);
   if (e != cudaSuccess) return e;
-  k_store_init<<<(N + 255) / 256, 256, 0, st>>>(mark, NW, D, N);
+  k_store_init<<<(L.N + 255) / 256, 256, 0, st>>>(L, mark, D);
   return cudaGetLastError();
 }
 
 // fill_from_tree on an arbitrary parent array (DistanceArray API).  out3 =
 // {new pairs, disagreements, cycle flag}.  Values within `tol` (relative)
 // agree; tol = 0 for integer images (exact, as the reference).
-__global__ void k_fill_tree_api(int N, int NW, const int* parent, const float* td,
-                                uint32_t* mark, int* cnt, float* D, unsigned long long* out3,
-                                float tol) {
+__global__ void k_fill_tree_api(MarkLayout L, const int* parent, const float* td, uint32_t* mark,
+                                int* cnt, float* D, unsigned long long* out3, float tol) {
+  const int N = L.N;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
     int u = parent[v];
     int steps = 0, lnew = 0, bad = 0;
     const float dv = td[v];
+    const uint32_t vcol = mcol(L, (uint32_t)v);
     while (u >= 0) {
       const float duv = __fsub_rn(dv, td[u]);
-      const uint32_t ubit = 1u << (u & 31);
-      uint32_t old = atomicOr(&mark[(size_t)v * NW + (u >> 5)], ubit);
+      const uint32_t ucol = mcol(L, (uint32_t)u);
+      const uint32_t ubit = 1u << (ucol & 31);
+      uint32_t old = atomicOr(&mark[mword(L, (uint32_t)v, ucol)], ubit);
       if (!(old & ubit)) {
-        atomicOr(&mark[(size_t)u * NW + (v >> 5)], 1u << (v & 31));
+        atomicOr(&mark[mword(L, (uint32_t)u, vcol)], 1u << (vcol & 31));
         D[(size_t)v * N + u] = duv;
         D[(size_t)u * N + v] = duv;
         atomicAdd(&cnt[u], 1);
@@ -289,28 +352,31 @@ __global__ void k_fill_tree_api(int N, int NW, const int* parent, const float* t
   }
 }
 
-cudaError_t launch_fill_tree_api(int N, int NW, const int* parent, const float* tdist,
+cudaError_t launch_fill_tree_api(const MarkLayout& L, const int* parent, const float* tdist,
                                  uint32_t* mark, int* cnt, float* D, unsigned long long* out3,
                                  float tol, cudaStream_t st) {
-  k_fill_tree_api<<<(N + 255) / 256, 256, 0, st>>>(N, NW, parent, tdist, mark, cnt, D, out3, tol);
+  k_fill_tree_api<<<(L.N + 255) / 256, 256, 0, st>>>(L, parent, tdist, mark, cnt, D, out3, tol);
   return cudaGetLastError();
 }
 
 // fill_from_source (distances.py:120-147): row and column of s.
-__global__ void k_fill_source_api(int N, int NW, int s, const float* dist, uint32_t* mark,
+__global__ void k_fill_source_api(MarkLayout L, int s, const float* dist, uint32_t* mark,
                                   int* cnt, float* D, unsigned long long* out3, float tol) {
+  const int N = L.N;
+  const uint32_t scol = mcol(L, (uint32_t)s);
   int lnew = 0, bad = 0;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < N; x += gridDim.x * blockDim.x) {
     if (x == s) continue;
-    const uint32_t xbit = 1u << (x & 31);
+    const uint32_t xcol = mcol(L, (uint32_t)x);
+    const uint32_t xbit = 1u << (xcol & 31);
     const float val = dist[x];
-    if (mark[(size_t)s * NW + (x >> 5)] & xbit) {
+    if (mark[mword(L, (uint32_t)s, xcol)] & xbit) {
       float cur = D[(size_t)s * N + x];
       if (fabsf(cur - val) > tol * fmaxf(fabsf(val), 1.0f)) bad++;
       continue;
     }
-    atomicOr(&mark[(size_t)s * NW + (x >> 5)], xbit);
-    atomicOr(&mark[(size_t)x * NW + (s >> 5)], 1u << (s & 31));
+    atomicOr(&mark[mword(L, (uint32_t)s, xcol)], xbit);
+    atomicOr(&mark[mword(L, (uint32_t)x, scol)], 1u << (scol & 31));
     D[(size_t)s * N + x] = val;
     D[(size_t)x * N + s] = val;
     atomicAdd(&cnt[x], 1);
@@ -320,25 +386,26 @@ __global__ void k_fill_source_api(int N, int NW, int s, const float* dist, uint3
   if (bad) atomicAdd(&out3[1], (unsigned long long)bad);
 }
 
-cudaError_t launch_fill_source_api(int N, int NW, int s, const float* dist, uint32_t* mark,
+cudaError_t launch_fill_source_api(const MarkLayout& L, int s, const float* dist, uint32_t* mark,
                                    int* cnt, float* D, unsigned long long* out3, float tol,
                                    cudaStream_t st) {
-  k_fill_source_api<<<(N + 255) / 256, 256, 0, st>>>(N, NW, s, dist, mark, cnt, D, out3, tol);
+  k_fill_source_api<<<(L.N + 255) / 256, 256, 0, st>>>(L, s, dist, mark, cnt, D, out3, tol);
   return cudaGetLastError();
 }
 
-__global__ void k_mark_unpack(const uint32_t* mark, int N, int NW, uint8_t* out) {
-  size_t total = (size_t)N * N;
+__global__ void k_mark_unpack(MarkLayout L, const uint32_t* mark, uint8_t* out) {
+  const size_t N = L.N, total = N * N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
-    size_t r = i / N, c = i % N;
-    out[i] = (mark[r * NW + (c >> 5)] >> (c & 31)) & 1u;
+    const uint32_t r = (uint32_t)(i / N), c = (uint32_t)(i % N);
+    const uint32_t ct = mcol(L, c);
+    out[i] = (mark[mword(L, r, ct)] >> (ct & 31)) & 1u;
   }
 }
 
-cudaError_t launch_mark_unpack(const uint32_t* mark, int N, int NW, uint8_t* out,
+cudaError_t launch_mark_unpack(const MarkLayout& L, const uint32_t* mark, uint8_t* out,
                                cudaStream_t st) {
-  k_mark_unpack<<<1184, 256, 0, st>>>(mark, N, NW, out);
+  k_mark_unpack<<<1184, 256, 0, st>>>(L, mark, out);
   return cudaGetLastError();
 }
 
@@ -347,23 +414,21 @@ cudaError_t launch_mark_unpack(const uint32_t* mark, int N, int NW, uint8_t* out
 // unmarked entries are exactly x > s, so the sequence is 0..N-2 and commit s
 // adds N-1-s pairs.  The batched naive propagation writes those rows; this
 // kernel sets the bookkeeping to the state the sequential loop ends in.
-__global__ void k_naive_trace(int N, int NW, uint32_t* mark, int* cnt, int* seq,
+__global__ void k_naive_trace(MarkLayout L, uint32_t* mark, int* cnt, int* seq,
                               unsigned long long* newp) {
+  const int N = L.N;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
     cnt[v] = N - 1;
     if (v < N - 1) { seq[v] = v; newp[v] = (unsigned long long)(N - 1 - v); }
-    uint32_t* row = mark + (size_t)v * NW;
-    for (int w = 0; w < NW; w++) {
-      int lo = w * 32;
-      int nb = min(32, N - lo);
-      row[w] = nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u);
-    }
   }
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)N * L.RW;
+       i += (size_t)gridDim.x * blockDim.x)
+    mark[i] = 0xFFFFFFFFu;
 }
 
-cudaError_t launch_naive_trace(int N, int NW, uint32_t* mark, int* cnt, int* seq,
+cudaError_t launch_naive_trace(const MarkLayout& L, uint32_t* mark, int* cnt, int* seq,
                                unsigned long long* newp, cudaStream_t st) {
-  k_naive_trace<<<(N + 255) / 256, 256, 0, st>>>(N, NW, mark, cnt, seq, newp);
+  k_naive_trace<<<592, 256, 0, st>>>(L, mark, cnt, seq, newp);
   return cudaGetLastError();
 }
 

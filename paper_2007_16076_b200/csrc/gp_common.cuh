@@ -51,7 +51,39 @@ __device__ __forceinline__ int parent_of(int v, uint8_t code, int W) {
   return code == GP_ROOT ? -1 : v + (code / 3 - 1) * W + (code % 3 - 1);
 }
 
-__device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) { return __ldcg(p); }
-__device__ __forceinline__ int ldcg_i32(const int* p) { return __ldcg(p); }
+// Column layout of the mark bitmap.  Row v holds the mark bits of pairs
+// (v, *).  Columns are ordered by 16x16 pixel tiles (tile-major, raster inside
+// a tile) so that the bits of a compact pixel region -- a subtree, tested
+// together by one warp -- share 32-byte sectors; one tile is one sector.
+// Images narrower or shorter than 16 use plain raster columns.
+struct MarkLayout {
+  int N;          // pixels
+  int W;          // image width (tiling)
+  int tiled;      // 16x16 tile order?
+  int RW;         // 32-bit words per row
+  int TWn;        // tiles per image row
+  uint32_t magic; // floor(2^32 / W) + 1: exact c / W for c, W < 2^16
+};
+
+__host__ __device__ inline MarkLayout make_layout(int N, int H, int W) {
+  MarkLayout L;
+  L.N = N;
+  L.W = W;
+  L.tiled = (H >= 16 && W >= 16) ? 1 : 0;
+  L.TWn = (W + 15) / 16;
+  L.RW = L.tiled ? ((H + 15) / 16) * L.TWn * 8 : (N + 31) / 32;
+  L.magic = L.tiled ? (uint32_t)((0x100000000ull / (unsigned long long)W) + 1ull) : 0u;
+  return L;
+}
+
+__device__ __forceinline__ uint32_t mcol(const MarkLayout& L, uint32_t c) {
+  if (!L.tiled) return c;
+  const uint32_t r = __umulhi(c, L.magic), cc = c - r * (uint32_t)L.W;
+  return (((r >> 4) * (uint32_t)L.TWn + (cc >> 4)) << 8) + ((r & 15u) << 4) + (cc & 15u);
+}
+
+__device__ __forceinline__ size_t mword(const MarkLayout& L, uint32_t row, uint32_t col_t) {
+  return (size_t)row * L.RW + (col_t >> 5);
+}
 
 }  // namespace gp

@@ -8,6 +8,26 @@
 
 namespace gp {
 
+// ---------------- tree store ----------------
+// One committed-or-speculative tree per slot, in Euler-tour (preorder) form:
+//   pre[q]   pixel at preorder position q (u16)
+//   szp[q]   number of descendants of pre[q] (u16)
+//   tdp[q]   geodesic distance of pre[q] from the root (fp32)
+//   part[p]  start of commit-warp p's share of the fill work, packed
+//            q | (chunk offset << 16); chunk = 32 consecutive descendants
+//   T        total chunks of the tree
+// desc(pre[q]) = pre[q+1 .. q+szp[q]], so the ancestor/descendant pairs of
+// the tree are the contiguous ranges of this array (no pointer chasing).
+struct TreeStore {
+  uint16_t* pre;
+  uint16_t* szp;
+  float* tdp;
+  uint32_t* part;
+  uint32_t* T;
+  int nparts;  // commit warps (partition count)
+  int cap;     // slots
+};
+
 // ---------------- K1 propagation ----------------
 struct PropArgs {
   Grid g;
@@ -15,20 +35,19 @@ struct PropArgs {
   const int* src;          // tree t uses src[t*ns .. t*ns+ns)
   int ns;                  // sources per tree
   const int* ntrees_dev;   // optional device tree count (CTAs >= count exit)
-  const int* slot;         // optional explicit output slot per tree
-  int* slot_counter;       // optional: allocate slots atomically ...
-  int* slot_of;            // ... and record slot_of[src] = slot
-  float* out_dist;         // [slot][N] (nullable)
-  uint8_t* out_dir;        // [slot][N] window codes, GP_ROOT for roots (nullable)
-  uint32_t* scratch;       // per-CTA scratch when the map does not fit smem
-  size_t scratch_words;
+  const int* slot;         // optional output slot per tree (default: t)
+  float* out_dist;         // [slot][N] pixel-order distances (nullable)
+  uint8_t* out_dir;        // [slot][N] parent window codes (nullable)
+  TreeStore ts;            // Euler-tour outputs (ts.pre == nullptr: none)
+  uint8_t* scratch;        // per-CTA scratch when the map does not fit smem
+  size_t scratch_bytes;
   int in_smem;
   float delta;             // bucket width (inf = plain frontier relaxation)
   float* D;                // naive epilogue: D row/col x > src (nullable)
 };
 
 size_t prop_smem_bytes(int N);
-size_t prop_scratch_words(int N);
+size_t prop_scratch_bytes(int N);
 bool prop_fits_smem(int N);
 cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st);
 
@@ -37,46 +56,50 @@ struct Ctl {
   int step;       // next step index
   int cur_src;    // selected source of `step` (-1: not selected yet, -2: none left)
   int status;     // CTL_*
-  int nslots;     // trees stored so far
+  int nslots;     // slots ever handed out (bump allocator)
   int ncand;      // candidates produced by the last top-K
-  int pad[3];
+  int free_top;   // free-slot stack height
+  int total_props; // trees propagated by speculative batches
+  int pad;
 };
 enum { CTL_RUNNING = 0, CTL_DONE = 1, CTL_MISS = 2, CTL_LIMIT = 3 };
 
 struct CommitArgs {
   Grid g;
+  MarkLayout L;
   int strategy;            // kNaive (naive_with_tree) or kFillingRate
-  int NW;                  // 32-bit words per mark row
-  const float* tdist;      // tree store [slot][N]
-  const uint8_t* tdir;     // tree store [slot][N]
-  const int* slot_of;      // [N] slot of a pixel's tree, -1 if none
-  uint32_t* mark;          // [N][NW] bitmap, bit (v,u) = row v, column u
+  TreeStore ts;
+  int* slot_of;            // [N] slot of a pixel's tree, -1 none, -2 committed
+  int* free_stack;         // [cap] recycled slots
+  uint32_t* mark;          // [N][RW] bitmap
   int* cnt;                // [N] marked off-diagonal entries per pixel
   float* D;                // [N][N]
   const int* rank;         // [N] position in the extrema ranking (filling-rate)
   const int* ext;          // [N] pixel at each rank
-  unsigned* selkey;        // [N+1] per-step selection key (atomicMin target)
+  unsigned* selkey;        // [N+2] per-step selection key (atomicMin target)
   int* seq;                // [N] committed sources
   unsigned long long* newp;// [N] new pairs per commit
   Ctl* ctl;
   int max_steps;           // commits allowed in this launch
 };
 
+constexpr int COMMIT_THREADS = 512;
 cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st);
 int commit_max_blocks();
-cudaError_t launch_topk(const CommitArgs& a, int K, int* cands, cudaStream_t st);
+cudaError_t launch_topk(const CommitArgs& a, int K, int* cands, int* slots, cudaStream_t st);
 
 // ---------------- store helpers ----------------
-cudaError_t launch_store_init(uint32_t* mark, int NW, float* D, int N, cudaStream_t st);
+cudaError_t launch_store_init(const MarkLayout& L, uint32_t* mark, float* D, cudaStream_t st);
 // API-level fills (explicit parent arrays; reference semantics incl. checks)
-cudaError_t launch_fill_tree_api(int N, int NW, const int* parent, const float* tdist,
+cudaError_t launch_fill_tree_api(const MarkLayout& L, const int* parent, const float* tdist,
                                  uint32_t* mark, int* cnt, float* D, unsigned long long* out3,
                                  float tol, cudaStream_t st);
-cudaError_t launch_fill_source_api(int N, int NW, int s, const float* dist, uint32_t* mark,
+cudaError_t launch_fill_source_api(const MarkLayout& L, int s, const float* dist, uint32_t* mark,
                                    int* cnt, float* D, unsigned long long* out3, float tol,
                                    cudaStream_t st);
-cudaError_t launch_mark_unpack(const uint32_t* mark, int N, int NW, uint8_t* out, cudaStream_t st);
-cudaError_t launch_naive_trace(int N, int NW, uint32_t* mark, int* cnt, int* seq,
+cudaError_t launch_mark_unpack(const MarkLayout& L, const uint32_t* mark, uint8_t* out,
+                               cudaStream_t st);
+cudaError_t launch_naive_trace(const MarkLayout& L, uint32_t* mark, int* cnt, int* seq,
                                unsigned long long* newp, cudaStream_t st);
 cudaError_t launch_argmax_first(const float* x, int N, int* out, cudaStream_t st);
 
