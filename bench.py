@@ -1,0 +1,320 @@
+"""Benchmark: filled pixel-pairs/s and ms per image on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one complete filling-rate (or naive, config 1) run over one
+synthetic image of the chosen BASELINE config: D is complete on the device at
+the end of the step.  `value` is whole-job pairs/s: N ranks each fill one
+replica image per step ("replicas only": the selection chain does not shard,
+see DESIGN.md), value = N * A * K / max-over-ranks(device time of K steps).
+
+* Device time of a step = CUDA events recorded by gp_run on its own stream
+  around the whole run (store reset, extrema, commit launches, speculative
+  propagation batches).  The image is resident on the device; L2 is flushed
+  (256 MiB write) between steps (D at config 2 is only 64 MiB).
+* e2e = the same metric through the C ABI with host buffers: per step
+  gp_ctx_load (validation + H2D of the image from pinned memory) + gp_run +
+  gp_store_read of D into pinned host memory (D2H 4*N^2 bytes); wall clock
+  around the synchronous calls.
+* roofline: dominant kernel = the commit loop (k_commit).  Algorithmic bytes
+  per image B_alg = 4N^2 + N^2/8 + C/4 + 10*N*P with C the
+  ancestor/descendant pairs of the committed trees (measured on device),
+  divided by the summed k_commit event time.
+* cpu_baseline / --impl reference: the oracle port (oracle/, C, OpenMP fill)
+  on the host cores, over a bounded prefix of the same run (the first M
+  commits of the GPU's own committed sequence, identical to the oracle's by
+  the parity tests); value = pairs filled by the prefix / prefix time, which
+  flatters the CPU (early commits fill the most pairs).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2007_16076_b200.configs import CONFIGS, make_image  # noqa: E402
+
+DEFAULT_CONFIG = 4
+METRIC = "filled pixel-pairs/sec and ms per image (1 B200); achieved HBM GB/s vs peak"
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _cpu_sample(img, spec, seq, target_s: float, nthreads: int):
+    """Oracle port over the first M commits of `seq` (~target_s seconds)."""
+    from oracle import oracle as O
+
+    use_tree = spec.strategy != "naive"
+    # grow the prefix geometrically until it takes >= target_s/2 (or is whole)
+    m = min(len(seq), 16)
+    while True:
+        t0 = time.perf_counter()
+        new = O.replay_prefix(img, seq, m, conn=spec.conn, use_tree=use_tree, nthreads=nthreads)
+        dt = time.perf_counter() - t0
+        if dt >= target_s / 2 or m >= len(seq):
+            break
+        m = min(len(seq), max(m + 1, int(m * min(8.0, target_s / max(dt, 1e-3)))))
+    pairs = int(new.sum())
+    return {
+        "value": pairs / dt, "unit": "pairs/s", "cores": nthreads, "kind": "port",
+        "sample": (f"oracle/oracle.c replay of the first {m} of {len(seq)} commits of the same "
+                   f"{spec.name} run ({pairs} of {spec.total_pairs} pairs in {dt:.2f}s); prefix "
+                   "rate flatters the CPU (early commits fill the most pairs)"),
+        "seconds": dt, "commits": m,
+    }
+
+
+def run_reference(args, spec, img, world, rank):
+    """--impl reference: the reference path's CPU implementation (oracle port)."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    nthreads = os.cpu_count() or 1
+    # the committed sequence from the oracle itself (bounded: compute it once
+    # for small configs, else from the committed golden)
+    gpath = os.path.join(ROOT, "tests", "golden", f"cfg{spec.index}.npz")
+    if os.path.exists(gpath):
+        seq = np.load(gpath)["seq"]
+    else:
+        seq = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads)["seq"]
+    per_step = 20.0
+    vals = []
+    samples = []
+    for i in range(args.warmup + args.steps):
+        r = _cpu_sample(img, spec, seq, per_step, nthreads)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            samples.append(r)
+    v = statistics.mean(vals)
+    ms = statistics.mean(s["seconds"] for s in samples) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if spec.dtype == "f32" else "f32(int-exact)",
+        "data": "synthetic", "config": {"workload": spec.name, "image": list(spec.shape),
+                                        "connectivity": spec.conn, "strategy": spec.strategy},
+        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": nthreads, "kind": "port",
+                         "sample": samples[-1]["sample"]},
+        "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    world, rank, local = _dist_env()
+    spec = CONFIGS[args.config]
+    img = make_image(args.config)
+
+    if args.impl == "reference":
+        run_reference(args, spec, img, world, rank)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2007_16076_b200 import _lib
+
+    L = _lib.load_library()
+    N = spec.n
+    A = spec.total_pairs
+    px = np.ascontiguousarray(img.astype(np.float32) if spec.dtype == "f32" else img)
+    dtype = _lib.DTYPE_F32 if spec.dtype == "f32" else _lib.DTYPE_U8
+    strat = _lib.STRATEGY_FILLING_RATE if spec.strategy == "filling-rate" else _lib.STRATEGY_NAIVE
+
+    def ctx_create():
+        h = ctypes.c_void_p()
+        _lib.check(L.gp_ctx_create(spec.shape[0], spec.shape[1], dtype, _lib.ptr(px), 1, spec.conn,
+                                   ctypes.byref(h)))
+        return h
+
+    ctx = ctx_create()
+    st = ctypes.c_void_p()
+    _lib.check(L.gp_store_create(N, ctypes.byref(st)))
+    seq = np.zeros(N, dtype=np.int32)
+    new = np.zeros(N, dtype=np.int64)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def one_run():
+        s = _lib.RunStats()
+        _lib.check(L.gp_run(ctx, st, strat, 0, 0, _lib.ptr(seq), _lib.ptr(new), ctypes.byref(s)))
+        return s
+
+    for _ in range(args.warmup):
+        one_run()
+        flush.zero_()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    runs = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            runs.append(one_run())
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = sum(r.ms_total for r in runs)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = world * A * args.steps / (total_ms / 1e3)
+    r0 = runs[-1]
+    P = int(r0.raw_count)
+    C = int(r0.visits)
+    commit_ms = statistics.mean(r.ms_commit for r in runs)
+    prop_ms = statistics.mean(r.ms_propagate for r in runs)
+
+    # ---- e2e through the C ABI with host buffers ----
+    Dh = torch.empty((N, N), dtype=torch.float32, pin_memory=True)
+    px_pinned = torch.from_numpy(px.copy()).pin_memory()
+    e2e_times = []
+    for i in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _lib.check(L.gp_ctx_load(ctx, dtype, ctypes.c_void_p(px_pinned.data_ptr())))
+        s2 = _lib.RunStats()
+        _lib.check(L.gp_run(ctx, st, strat, 0, 0, _lib.ptr(seq), _lib.ptr(new), ctypes.byref(s2)))
+        _lib.check(L.gp_store_read(st, ctypes.c_void_p(Dh.data_ptr()), None))
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = statistics.mean(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    # ---- roofline of the dominant kernel (commit loop) ----
+    peak, peak_kind = _peaks()
+    b_alg = 4.0 * N * N + N * N / 8.0 + C / 4.0 + 10.0 * N * P
+    achieved = b_alg / (commit_ms / 1e3) / 1e9 if commit_ms > 0 else 0.0
+    if spec.strategy == "naive":
+        b_alg = 4.0 * N * N + N * N / 8.0 + 10.0 * N * P
+        achieved = b_alg / (prop_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if spec.dtype == "f32" else "f32 (integer-exact)",
+        "data": "synthetic (seeded generator, paper_2007_16076_b200/configs.py)",
+        "config": {"workload": spec.name, "image": list(spec.shape), "connectivity": spec.conn,
+                   "strategy": spec.strategy, "pairs_per_image": A, "propagations_raw": P,
+                   "propagations_adjusted": int(r0.adjusted_count),
+                   "parallelism": f"replicas x{world}", "l2": "flushed (256 MiB write) between steps"},
+        "e2e": {"value": world * A / e2e_s, "unit": "pairs/s", "ms_per_image": e2e_s * 1e3,
+                "h2d_bytes_per_step": int(px.nbytes), "d2h_bytes_per_step": 4 * N * N},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "k_commit" if spec.strategy != "naive" else "k_propagate",
+                     "algorithmic_bytes_per_image": b_alg, "C_visits": C,
+                     "kernel_ms_per_image": commit_ms if spec.strategy != "naive" else prop_ms},
+        "breakdown_ms": {"commit": commit_ms, "propagate": prop_ms,
+                         "setup": statistics.mean(r.ms_setup for r in runs),
+                         "batches": int(r0.batches), "trees": int(r0.propagations)},
+        "gpu_launches": int(sum(r.kernels for r in runs)),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = _cpu_sample(img, spec, seq[:P].copy(), args.cpu_seconds,
+                                           os.cpu_count() or 1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    L.gp_store_destroy(st)
+    L.gp_ctx_destroy(ctx)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -12,6 +12,7 @@
  *
  *   gp_ctx_create        GridGraph.__init__ / _build_csr   propagation.py:52-56,67-89
  *                        (+ Image validation grid.py:47-60)
+ *   gp_ctx_load          (new) new image into an existing context
  *   gp_propagate         GridGraph.propagate -> dijkstra_csr propagation.py:58-64,
  *                                                            _kernels.py:33-79
  *   gp_propagate_batch   (new) K independent single-source propagations into a
@@ -64,6 +65,8 @@ typedef struct {
   int64_t launches;        /* commit-kernel launches */
   int64_t kernels;         /* total kernels launched by the run */
   int64_t filled_pairs;    /* sum of new pairs (== A on completion) */
+  int64_t visits;          /* ancestor/descendant pairs of the committed trees
+                              (sum of depths, C); 0 for naive */
   double ms_total;         /* device time of the run (CUDA events) */
   double ms_propagate;     /* device time inside propagation batches */
   double ms_commit;        /* device time inside commit launches */
@@ -78,6 +81,9 @@ int gp_version(void);
  * (additive extension).  conn: 8 (reference) or 4 (additive extension). */
 int gp_ctx_create(int H, int W, int dtype, const void *pixels, int metric, int conn,
                   gp_ctx **out);
+/* Replace the image of an existing context (same shape/metric/connectivity),
+ * keeping its device allocations -- for streams of images. */
+int gp_ctx_load(gp_ctx *ctx, int dtype, const void *pixels);
 void gp_ctx_destroy(gp_ctx *ctx);
 int gp_ctx_num_pixels(const gp_ctx *ctx);
 

@@ -19,7 +19,8 @@ STRATEGY_NAIVE, STRATEGY_FILLING_RATE = 0, 1
 
 # every symbol declared in include/geopairs_b200.h
 EXPORTS = (
-    "gp_last_error", "gp_version", "gp_ctx_create", "gp_ctx_destroy", "gp_ctx_num_pixels",
+    "gp_last_error", "gp_version", "gp_ctx_create", "gp_ctx_load", "gp_ctx_destroy",
+    "gp_ctx_num_pixels",
     "gp_propagate", "gp_propagate_batch", "gp_extrema", "gp_store_create", "gp_store_destroy",
     "gp_store_device_ptrs", "gp_store_fill_tree", "gp_store_fill_source", "gp_store_counts",
     "gp_store_read", "gp_run",
@@ -31,7 +32,7 @@ class RunStats(ctypes.Structure):
         ("raw_count", ctypes.c_int64), ("adjusted_count", ctypes.c_int64),
         ("centroid", ctypes.c_int64), ("propagations", ctypes.c_int64),
         ("batches", ctypes.c_int64), ("launches", ctypes.c_int64),
-        ("kernels", ctypes.c_int64), ("filled_pairs", ctypes.c_int64),
+        ("kernels", ctypes.c_int64), ("filled_pairs", ctypes.c_int64), ("visits", ctypes.c_int64),
         ("ms_total", ctypes.c_double), ("ms_propagate", ctypes.c_double),
         ("ms_commit", ctypes.c_double), ("ms_setup", ctypes.c_double),
     ]
@@ -61,6 +62,7 @@ def load_library(path: str = LIB_PATH, *, require_device: bool = True):
     P, i32, i64, f32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float
     L.gp_last_error.restype = ctypes.c_char_p
     L.gp_ctx_create.argtypes = [i32, i32, i32, P, i32, i32, ctypes.POINTER(P)]
+    L.gp_ctx_load.argtypes = [P, i32, P]
     L.gp_ctx_destroy.argtypes = [P]
     L.gp_ctx_destroy.restype = None
     L.gp_ctx_num_pixels.argtypes = [P]

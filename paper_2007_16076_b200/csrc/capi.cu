@@ -45,6 +45,7 @@ struct gp_ctx {
   uint8_t* scratch = nullptr;
   size_t scratch_trees = 0;
   int commit_blocks = 0;
+  double mean_w = 1.0;  // mean edge weight (bucket width scale)
 };
 
 struct gp_store {
@@ -67,15 +68,11 @@ static cudaError_t dalloc(T** p, size_t count) {
   return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T) + 16);
 }
 
-extern "C" int gp_ctx_create(int H, int W, int dtype, const void* pixels, int metric, int conn,
-                             gp_ctx** out) {
-  if (!out || !pixels) return fail(GP_EINVAL, "null argument");
-  if (H < 1 || W < 1 || (int64_t)H * W < 2) return fail(GP_EINVAL, "image must contain at least 2 pixels");
-  if ((int64_t)H * W > 65536) return fail(GP_EINVAL, "images above 65536 pixels are not supported (dense N^2 store)");
-  if (conn != 4 && conn != 8) return fail(GP_EINVAL, "connectivity must be 4 or 8");
-  if (metric < 0 || metric > 2) return fail(GP_EINVAL, "unknown metric");
+// Validate + convert host pixels to fp32 (grid.py:47-60 semantics).
+static int convert_pixels(int H, int W, int dtype, const void* pixels, int metric, int conn,
+                          std::vector<float>& f, int* isint_out) {
   const int N = H * W;
-  std::vector<float> f(N);
+  f.resize(N);
   int isint = dtype != GP_DTYPE_F32;
   double vmax = 0.0;
   for (int i = 0; i < N; i++) {
@@ -97,9 +94,34 @@ extern "C" int gp_ctx_create(int H, int W, int dtype, const void* pixels, int me
     double wmax = metric == GP_METRIC_MEAN ? 2 * vmax : 4 * vmax;
     if (wmax * hops >= 16777216.0) return fail(GP_EINVAL, "integer distances would exceed 2^24");
   }
+  *isint_out = isint;
+  return GP_OK;
+}
+
+static double mean_weight(const std::vector<float>& f, int metric) {
+  double s = 0;
+  for (float v : f) s += v;
+  double m = f.empty() ? 1.0 : s / f.size();
+  double w = metric == GP_METRIC_SUM ? 4 * m : metric == GP_METRIC_MEAN ? 2 * m : m;
+  return w > 0 ? w : 1.0;
+}
+
+extern "C" int gp_ctx_create(int H, int W, int dtype, const void* pixels, int metric, int conn,
+                             gp_ctx** out) {
+  if (!out || !pixels) return fail(GP_EINVAL, "null argument");
+  if (H < 1 || W < 1 || (int64_t)H * W < 2) return fail(GP_EINVAL, "image must contain at least 2 pixels");
+  if ((int64_t)H * W > 65536) return fail(GP_EINVAL, "images above 65536 pixels are not supported (dense N^2 store)");
+  if (conn != 4 && conn != 8) return fail(GP_EINVAL, "connectivity must be 4 or 8");
+  if (metric < 0 || metric > 2) return fail(GP_EINVAL, "unknown metric");
+  const int N = H * W;
+  std::vector<float> f;
+  int isint = 0;
+  int rc = convert_pixels(H, W, dtype, pixels, metric, conn, f, &isint);
+  if (rc) return rc;
   gp_ctx* c = new gp_ctx();
   c->g = Grid{H, W, N, conn, metric};
   c->isint = isint;
+  c->mean_w = mean_weight(f, metric);
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -114,6 +136,19 @@ extern "C" int gp_ctx_create(int H, int W, int dtype, const void* pixels, int me
   return GP_OK;
 }
 
+extern "C" int gp_ctx_load(gp_ctx* c, int dtype, const void* pixels) {
+  if (!c || !pixels) return fail(GP_EINVAL, "null argument");
+  std::vector<float> f;
+  int isint = 0;
+  int rc = convert_pixels(c->g.H, c->g.W, dtype, pixels, c->g.metric, c->g.conn, f, &isint);
+  if (rc) return rc;
+  c->isint = isint;
+  c->mean_w = mean_weight(f, c->g.metric);
+  CUDA_TRY(cudaMemcpyAsync(c->d_img, f.data(), (size_t)c->g.N * 4, cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return GP_OK;
+}
+
 extern "C" void gp_ctx_destroy(gp_ctx* c) {
   if (!c) return;
   cudaFree(c->d_img);
@@ -122,6 +157,7 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
   cudaFree(c->ts.tdp);
   cudaFree(c->ts.part);
   cudaFree(c->ts.T);
+  cudaFree(c->ts.C);
   cudaFree(c->scratch);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
@@ -149,9 +185,13 @@ static PropArgs base_prop(gp_ctx* c) {
   return a;
 }
 
+// Bucket width of the propagation (K1): a multiple of the mean edge weight
+// (GP_DELTA_FACTOR, default below; <= 0 or "inf" = unbucketed frontier).
 static float default_delta(const gp_ctx* c) {
-  (void)c;
-  return INFINITY;
+  double factor = 4.0;
+  if (const char* e = getenv("GP_DELTA_FACTOR")) factor = atof(e);
+  if (!(factor > 0) || std::isinf(factor)) return INFINITY;
+  return (float)(factor * c->mean_w);
 }
 
 extern "C" int gp_propagate(gp_ctx* c, const int32_t* sources, int nsrc, float* dist_out,
@@ -423,6 +463,7 @@ static int ensure_tree_store(gp_ctx* c, int nparts) {
   const int N = c->g.N;
   if (c->ts.pre && c->ts.cap >= N && c->ts.nparts == nparts) return GP_OK;
   cudaFree(c->ts.pre); cudaFree(c->ts.szp); cudaFree(c->ts.tdp); cudaFree(c->ts.part); cudaFree(c->ts.T);
+  cudaFree(c->ts.C);
   c->ts = TreeStore{};
   const size_t cap = (size_t)N;  // a pixel is propagated at most once: N slots always suffice
   CUDA_TRY(dalloc(&c->ts.pre, cap * N));
@@ -430,6 +471,7 @@ static int ensure_tree_store(gp_ctx* c, int nparts) {
   CUDA_TRY(dalloc(&c->ts.tdp, cap * N));
   CUDA_TRY(dalloc(&c->ts.part, cap * nparts));
   CUDA_TRY(dalloc(&c->ts.T, cap));
+  CUDA_TRY(dalloc(&c->ts.C, cap));
   c->ts.cap = (int)cap;
   c->ts.nparts = nparts;
   return GP_OK;
@@ -561,6 +603,8 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     }
     CUDA_TRY(cudaEventRecord(setup.b, st));
     int K = spec_k > 0 ? spec_k : 2 * c->nsm;
+    if (spec_k <= 0)
+      if (const char* e = getenv("GP_SPEC_K")) K = atoi(e);
     K = std::min(K, N);
     CUDA_TRY(dalloc(&d_cands, K));
     CUDA_TRY(dalloc(&d_slots, K));
@@ -591,8 +635,31 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     pa.slot = d_slots;
     pa.ts = c->ts;
     pa.delta = default_delta(c);
+    // debug phase stamps (GP_DEBUG=1): per tree of the batches, per step
+    const bool debug = getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"));
+    unsigned long long *d_pdbg = nullptr, *d_cdbg = nullptr;
+    std::vector<unsigned long long> pdbg_acc(8, 0);
+    long long pdbg_n = 0;
+    if (debug) {
+      CUDA_TRY(dalloc(&d_pdbg, (size_t)K * 8));
+      CUDA_TRY(dalloc(&d_cdbg, (size_t)(N + 2) * 4));
+      CUDA_TRY(cudaMemsetAsync(d_cdbg, 0, (size_t)(N + 2) * 32, st));
+      pa.dbg = d_pdbg;
+      ca.dbg = d_cdbg;
+    }
     std::vector<EvPair> pev, cev;
     for (int guard = 0; guard < 4 * N + 8; guard++) {
+      if (debug && guard > 0) {  // fold the previous batch's stamps
+        std::vector<unsigned long long> h((size_t)K * 8);
+        CUDA_TRY(cudaMemcpy(h.data(), d_pdbg, h.size() * 8, cudaMemcpyDeviceToHost));
+        for (int t = 0; t < std::min(K, h_ctl.ncand); t++) {
+          unsigned long long* r = &h[(size_t)t * 8];
+          for (int j = 1; j <= 5; j++) pdbg_acc[j] += r[j] - r[j - 1];
+          pdbg_acc[6] += r[6];
+          pdbg_acc[7] += r[7];
+          pdbg_n++;
+        }
+      }
       EvPair e;
       cudaEventCreate(&e.a); cudaEventCreate(&e.b);
       CUDA_TRY(cudaEventRecord(e.a, st));
@@ -618,12 +685,40 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     CUDA_TRY(cudaEventRecord(tot.b, st));
     CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (debug) {
+      std::vector<unsigned long long> h((size_t)(N + 2) * 4);
+      CUDA_TRY(cudaMemcpy(h.data(), d_cdbg, h.size() * 8, cudaMemcpyDeviceToHost));
+      std::vector<double> ph[4];
+      for (int i = 0; i + 1 < h_ctl.step; i++) {
+        unsigned long long* r = &h[(size_t)i * 4];
+        unsigned long long* r2 = &h[(size_t)(i + 1) * 4];
+        if (!r[0] || !r2[0]) continue;
+        ph[0].push_back(r[1] - r[0]); ph[1].push_back(r[2] - r[1]);
+        ph[2].push_back(r[3] - r[2]); ph[3].push_back(r2[0] - r[3]);
+      }
+      auto med = [](std::vector<double>& v) {
+        if (v.empty()) return 0.0;
+        std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+        return v[v.size() / 2] / 1e3;
+      };
+      if (!ph[0].empty())
+        fprintf(stderr, "[gp debug] commit per step, median (us): fill(warp0) %.2f +rest-of-fill+barrier %.2f select %.2f barrier+next %.2f (n=%zu)\n",
+                med(ph[0]), med(ph[1]), med(ph[2]), med(ph[3]), ph[0].size());
+      if (pdbg_n)
+        fprintf(stderr, "[gp debug] propagate per tree (us): relax %.1f parents %.1f jump %.1f levels %.1f out %.1f | passes %.1f items/N %.2f (trees=%lld)\n",
+                pdbg_acc[1] / 1e3 / pdbg_n, pdbg_acc[2] / 1e3 / pdbg_n, pdbg_acc[3] / 1e3 / pdbg_n,
+                pdbg_acc[4] / 1e3 / pdbg_n, pdbg_acc[5] / 1e3 / pdbg_n, (double)pdbg_acc[6] / pdbg_n,
+                (double)pdbg_acc[7] / pdbg_n / N, pdbg_n);
+      cudaFree(d_pdbg);
+      cudaFree(d_cdbg);
+    }
     for (auto& e : cev) { S.ms_commit += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (auto& e : pev) { S.ms_propagate += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     P = h_ctl.step;
     cudaFree(d_slot_of); cudaFree(d_rank); cudaFree(d_ext); cudaFree(d_cands); cudaFree(d_slots);
     cudaFree(d_selkey); cudaFree(d_ctl); cudaFree(d_dfc); cudaFree(d_free);
     S.propagations += h_ctl.total_props;
+    S.visits = (int64_t)h_ctl.visits;
   }
   S.ms_total = ev_ms(tot);
   S.ms_setup = ev_ms(setup);

@@ -92,6 +92,14 @@ __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned* r
 }
 
 // K2 for one committed tree: this warp's share of the chunks.
+//
+// The warp walks its chunk range window by window: one coalesced load brings
+// the metadata of 32 consecutive preorder positions (descendant count, pixel,
+// distance, full-row flag), a warp scan of the chunk counts maps chunks to
+// positions, and the chunks are then processed G at a time so that the G
+// descendant-list loads and the G mark-word loads are each in flight
+// together (the fill is latency-bound: ~2 L2 round trips per G chunks).
+template <int G>
 __device__ __forceinline__ unsigned fill_warp_share(const CommitArgs& a, int slot, int s) {
   const int N = a.g.N;
   const int lane = threadIdx.x & 31;
@@ -112,61 +120,86 @@ __device__ __forceinline__ unsigned fill_warp_share(const CommitArgs& a, int slo
   unsigned total_new = 0;
   const MarkLayout L = a.L;
   while (count) {
-    unsigned sz = __ldg(&szp[q]);
-    if (sz == 0) {  // leaves carry no chunk: jump to the next internal node
-      for (;;) {
-        const int qq = q + lane;
-        const unsigned zz = qq < N ? (unsigned)__ldg(&szp[qq]) : 1u;
-        const unsigned m = __ballot_sync(0xffffffffu, zz != 0);
-        if (m) {
-          q += __ffs(m) - 1;
-          break;
-        }
-        q += 32;
-      }
-      sz = __ldg(&szp[q]);
+    // ---- window metadata, one position per lane ----
+    const int qa = q + lane;
+    unsigned sz_l = 0;
+    int u_l = 0;
+    float td_l = 0.f;
+    if (qa < N) {
+      sz_l = __ldg(&szp[qa]);
+      u_l = __ldg(&pre[qa]);
+      td_l = __ldg(&tdp[qa]);
     }
-    const unsigned nch = (sz + 31u) >> 5;
-    const unsigned take = min(nch - coff, count);
-    const int u = __ldg(&pre[q]);
-    const bool skip = (u != s) && (__ldcg(&a.cnt[u]) >= N - 1);  // full row: all set
-    if (!skip) {
-      const uint32_t ucol = mcol(L, (uint32_t)u);
-      const uint32_t ubit = 1u << (ucol & 31);
-      const float tdu = __ldg(&tdp[q]);
-      uint32_t* mrow = a.mark + (size_t)u * L.RW;
-      unsigned unew = 0;
-      for (unsigned c = coff; c < coff + take; c++) {
-        const unsigned k = c * 32u + lane;
-        if (k < sz) {
-          const int w = __ldg(&pre[q + 1 + k]);
-          const uint32_t wcol = mcol(L, (uint32_t)w);
-          const uint32_t wbit = 1u << (wcol & 31);
-          uint32_t* mw = mrow + (wcol >> 5);
-          if (!(__ldcg(mw) & wbit)) {
-            atomicOr(mw, wbit);
-            atomicOr(a.mark + mword(L, (uint32_t)w, ucol), ubit);
-            const float duv = __fsub_rn(__ldg(&tdp[q + 1 + k]), tdu);
-            a.D[(size_t)u * N + w] = duv;
-            a.D[(size_t)w * N + u] = duv;
-            atomicAdd(&a.cnt[w], 1);
-            unew++;
-          }
-        }
+    unsigned nch_l = (sz_l + 31u) >> 5;
+    unsigned c0_l = 0;
+    if (lane == 0) { nch_l -= coff; c0_l = coff; }
+    const bool full_l = nch_l && u_l != s && __ldcg(&a.cnt[u_l]) >= N - 1;
+    unsigned cum = nch_l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, cum, o);
+      if (lane >= o) cum += y;
+    }
+    const unsigned excl = cum - nch_l;
+    const unsigned wtotal = __shfl_sync(0xffffffffu, cum, 31);
+    const unsigned take = min(wtotal, count);
+    // ---- chunks, G at a time ----
+    for (unsigned cb = 0; cb < take; cb += G) {
+      int w[G], qc[G], uu[G];
+      bool ok[G];
+      float tdu[G];
+#pragma unroll
+      for (int j = 0; j < G; j++) {
+        const unsigned c = cb + j;
+        const unsigned m = __ballot_sync(0xffffffffu, cum > c);
+        const int ol = m ? __ffs(m) - 1 : 0;
+        const unsigned sz = __shfl_sync(0xffffffffu, sz_l, ol);
+        const unsigned cidx = __shfl_sync(0xffffffffu, c0_l + (c - excl), ol);
+        const bool full = __shfl_sync(0xffffffffu, (int)full_l, ol);
+        uu[j] = __shfl_sync(0xffffffffu, u_l, ol);
+        tdu[j] = __shfl_sync(0xffffffffu, td_l, ol);
+        qc[j] = q + ol;
+        const unsigned k = cidx * 32u + lane;
+        ok[j] = c < take && !full && k < sz;
+        w[j] = ok[j] ? (int)__ldg(&pre[qc[j] + 1 + k]) : 0;
+        qc[j] += 1 + (int)k;  // preorder position of w
+      }
+      uint32_t word[G], wbit[G];
+      uint32_t* mw[G];
+#pragma unroll
+      for (int j = 0; j < G; j++) {
+        const uint32_t wcol = mcol(L, (uint32_t)w[j]);
+        wbit[j] = 1u << (wcol & 31);
+        mw[j] = a.mark + (size_t)uu[j] * L.RW + (wcol >> 5);
+        word[j] = ok[j] ? __ldcg(mw[j]) : wbit[j];
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) unew += __shfl_xor_sync(0xffffffffu, unew, o);
-      if (lane == 0 && unew && u != s) atomicAdd(&a.cnt[u], (int)unew);
-      total_new += unew;
+      for (int j = 0; j < G; j++) {
+        const bool isnew = !(word[j] & wbit[j]);
+        if (isnew) {
+          const int u = uu[j], ww = w[j];
+          const uint32_t ucol = mcol(L, (uint32_t)u);
+          atomicOr(mw[j], wbit[j]);
+          atomicOr(a.mark + mword(L, (uint32_t)ww, ucol), 1u << (ucol & 31));
+          const float duv = __fsub_rn(__ldg(&tdp[qc[j]]), tdu[j]);
+          a.D[(size_t)u * N + ww] = duv;
+          a.D[(size_t)ww * N + u] = duv;
+          atomicAdd(&a.cnt[ww], 1);
+        }
+        const unsigned nb = __popc(__ballot_sync(0xffffffffu, isnew));
+        if (lane == 0 && nb && uu[j] != s) atomicAdd(&a.cnt[uu[j]], (int)nb);
+        total_new += nb;
+      }
     }
     count -= take;
-    q++;
+    q += 32;
     coff = 0;
   }
   return lane == 0 ? total_new : 0u;
 }
 
-__global__ void __launch_bounds__(COMMIT_THREADS) k_commit(CommitArgs a) {
+template <int G, int MINB>
+__global__ void __launch_bounds__(COMMIT_THREADS, MINB) k_commit(CommitArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned red32[32];
   __shared__ unsigned long long red64[32];
@@ -189,19 +222,25 @@ __global__ void __launch_bounds__(COMMIT_THREADS) k_commit(CommitArgs a) {
     const int slot = __ldcg(&a.slot_of[s]);
     if (slot < 0) { status = CTL_MISS; break; }
 
+    unsigned long long* dbg = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + (size_t)step * 4 : nullptr;
+    if (dbg) dbg[0] = gtimer();
     // ---- K2: Euler-range fill ----
-    unsigned long long lnew = fill_warp_share(a, slot, s);
+    unsigned long long lnew = fill_warp_share<G>(a, slot, s);
+    if (dbg) dbg[1] = gtimer();
     lnew = block_reduce_sum(lnew, red64);
     if (threadIdx.x == 0 && lnew) atomicAdd(&a.newp[step], lnew);
     grid.sync();
+    if (dbg) dbg[2] = gtimer();
     if (gtid == 0) {
       a.cnt[s] = N - 1;  // the root pairs with every pixel
       a.seq[step] = s;
       a.slot_of[s] = -2;  // committed: recycle the slot
+      a.ctl->visits += __ldg(&a.ts.C[slot]);
       a.free_stack[a.ctl->free_top++] = slot;
     }
     // ---- K3: selection of the next source ----
     select_step(a, step + 1, s, red32);
+    if (dbg) dbg[3] = gtimer();
     grid.sync();
     const unsigned key = __ldcg(&a.selkey[step + 1]);
     step++;
@@ -215,19 +254,32 @@ __global__ void __launch_bounds__(COMMIT_THREADS) k_commit(CommitArgs a) {
   }
 }
 
+// Fill pipelining depth G (chunks in flight per warp): G=4 keeps 2 CTAs of
+// 512 threads per SM within 64 registers; G=8 needs ~128 registers (1 CTA/SM).
+static const void* commit_kernel(int G) {
+  return G >= 8 ? (const void*)k_commit<8, 1> : (const void*)k_commit<4, 2>;
+}
+
+int commit_fill_depth() {
+  int G = 4;
+  if (const char* e = getenv("GP_FILL_G")) G = atoi(e);
+  return G >= 8 ? 8 : 4;
+}
+
 int commit_max_blocks() {
   int dev = 0, nsm = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_commit, COMMIT_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, commit_kernel(commit_fill_depth()),
+                                                COMMIT_THREADS, 0);
   return nsm * (per_sm > 0 ? per_sm : 1);
 }
 
 cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st) {
   CommitArgs args = a;
   void* params[] = {&args};
-  return cudaLaunchCooperativeKernel((void*)k_commit, dim3(num_blocks), dim3(COMMIT_THREADS),
-                                     params, 0, st);
+  return cudaLaunchCooperativeKernel(commit_kernel(commit_fill_depth()), dim3(num_blocks),
+                                     dim3(COMMIT_THREADS), params, 0, st);
 }
 
 // ---- speculative candidate batch: the K smallest keys among open pixels

@@ -86,4 +86,10 @@ __device__ __forceinline__ size_t mword(const MarkLayout& L, uint32_t row, uint3
   return (size_t)row * L.RW + (col_t >> 5);
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 }  // namespace gp

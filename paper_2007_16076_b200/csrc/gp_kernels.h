@@ -24,6 +24,7 @@ struct TreeStore {
   float* tdp;
   uint32_t* part;
   uint32_t* T;
+  uint32_t* C;  // ancestor/descendant pairs of the tree = sum of depths
   int nparts;  // commit warps (partition count)
   int cap;     // slots
 };
@@ -44,6 +45,7 @@ struct PropArgs {
   int in_smem;
   float delta;             // bucket width (inf = plain frontier relaxation)
   float* D;                // naive epilogue: D row/col x > src (nullable)
+  unsigned long long* dbg; // optional per-tree phase stamps [ntrees][8] (debug)
 };
 
 size_t prop_smem_bytes(int N);
@@ -61,6 +63,7 @@ struct Ctl {
   int free_top;   // free-slot stack height
   int total_props; // trees propagated by speculative batches
   int pad;
+  unsigned long long visits;  // sum of C over committed trees
 };
 enum { CTL_RUNNING = 0, CTL_DONE = 1, CTL_MISS = 2, CTL_LIMIT = 3 };
 
@@ -81,11 +84,13 @@ struct CommitArgs {
   unsigned long long* newp;// [N] new pairs per commit
   Ctl* ctl;
   int max_steps;           // commits allowed in this launch
+  unsigned long long* dbg; // optional per-step stamps [steps][4] from block 0 (debug)
 };
 
 constexpr int COMMIT_THREADS = 512;
 cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st);
 int commit_max_blocks();
+int commit_fill_depth();
 cudaError_t launch_topk(const CommitArgs& a, int K, int* cands, int* slots, cudaStream_t st);
 
 // ---------------- store helpers ----------------

@@ -13,6 +13,7 @@ import hashlib
 
 import numpy as np
 import pytest
+import torch
 
 from conftest import load_golden, small_cases
 from paper_2007_16076_b200.configs import CONFIGS, make_image
@@ -96,21 +97,32 @@ def _digest(D, isf):
     return hashlib.sha256(np.ascontiguousarray(D).astype("<f4" if isf else "<i4").tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("index", [1, 2])
+@pytest.mark.parametrize("index", [1, 2, 3, 4, 5])
 def test_config_matches_golden(gp, index):
     spec = CONFIGS[index]
     g = load_golden(f"cfg{index}.npz")
     img = make_image(index)
     kind = gp.StrategyKind.FILLING_RATE if spec.strategy == "filling-rate" else gp.StrategyKind.NAIVE
-    run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, kind, connectivity=spec.conn)
+    run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, kind, connectivity=spec.conn, force=True)
     seq = np.array([s for _, s, _ in run.trace.samples])
     assert run.trace.raw_count == int(g["raw"])
     assert run.trace.adjusted_count == int(g["adjusted"])
     assert np.array_equal(seq, g["seq"])
+    assert np.array_equal(run.distances.point_filled_counts, np.full(spec.n, spec.n - 1))
     isf = spec.dtype == "f32"
-    D = run.distances.dist_device().cpu().numpy()
-    assert np.allclose(D[g["samp_i"], g["samp_j"]], g["samp_v"], rtol=RTOL, atol=0)
-    assert _digest(D, isf) == str(g["d_sha256"])
+    Dd = run.distances.dist_device()
+    si = torch.as_tensor(g["samp_i"].astype(np.int64), device=Dd.device)
+    sj = torch.as_tensor(g["samp_j"].astype(np.int64), device=Dd.device)
+    samp = Dd[si, sj].cpu().numpy()
+    assert np.allclose(samp, g["samp_v"], rtol=RTOL, atol=0)
+    assert np.array_equal(samp, g["samp_v"].astype(np.float32))  # expected bit-exact
+    # size-independent properties at full size: symmetry, zero diagonal, row checksums
+    assert bool((Dd == Dd.T).all())
+    assert bool((torch.diagonal(Dd) == 0).all())
+    rows = torch.sum(Dd, dim=1, dtype=torch.float64).cpu().numpy()
+    assert np.allclose(rows, g["row_sum"], rtol=1e-9, atol=0)
+    if spec.n <= 16384:
+        assert _digest(Dd.cpu().numpy(), isf) == str(g["d_sha256"])
 
 
 def test_api_known_answers(gp):
