@@ -46,7 +46,7 @@ import numpy as np  # noqa: E402
 
 from paper_2007_16076_b200.configs import CONFIGS, make_image  # noqa: E402
 
-DEFAULT_CONFIG = 4
+DEFAULT_CONFIG = 5
 METRIC = "filled pixel-pairs/sec and ms per image (1 B200); achieved HBM GB/s vs peak"
 
 
@@ -112,27 +112,24 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def _cpu_sample(img, spec, seq, target_s: float, nthreads: int):
-    """Oracle port over the first M commits of `seq` (~target_s seconds)."""
+def _cpu_sample(img, spec, target_s: float, nthreads: int):
+    """The oracle port's real loop (selection + propagation + fill) for the
+    first M commits of the run, timed inside the loop (allocation excluded)."""
     from oracle import oracle as O
 
-    use_tree = spec.strategy != "naive"
-    # grow the prefix geometrically until it takes >= target_s/2 (or is whole)
-    m = min(len(seq), 16)
-    while True:
-        t0 = time.perf_counter()
-        new = O.replay_prefix(img, seq, m, conn=spec.conn, use_tree=use_tree, nthreads=nthreads)
-        dt = time.perf_counter() - t0
-        if dt >= target_s / 2 or m >= len(seq):
-            break
-        m = min(len(seq), max(m + 1, int(m * min(8.0, target_s / max(dt, 1e-3)))))
-    pairs = int(new.sum())
+    m = min(spec.n, 8)
+    r = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m)
+    per = r["loop_seconds"] / max(r["raw"], 1)
+    m = int(min(spec.n, max(m, target_s / max(per, 1e-6))))
+    r = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m)
+    dt, pairs = r["loop_seconds"], r["filled"]
     return {
         "value": pairs / dt, "unit": "pairs/s", "cores": nthreads, "kind": "port",
-        "sample": (f"oracle/oracle.c replay of the first {m} of {len(seq)} commits of the same "
-                   f"{spec.name} run ({pairs} of {spec.total_pairs} pairs in {dt:.2f}s); prefix "
-                   "rate flatters the CPU (early commits fill the most pairs)"),
-        "seconds": dt, "commits": m,
+        "sample": (f"oracle/oracle.c (C restatement of the reference loop, OpenMP fill) running the "
+                   f"first {r['raw']} commits of the {spec.name} filling-rate run: {pairs} of "
+                   f"{spec.total_pairs} pairs in {dt:.2f}s; the prefix rate flatters the CPU "
+                   "(early commits fill the most pairs)"),
+        "seconds": dt, "commits": int(r["raw"]),
     }
 
 
@@ -140,21 +137,12 @@ def run_reference(args, spec, img, world, rank):
     """--impl reference: the reference path's CPU implementation (oracle port)."""
     if rank != 0:
         return
-    from oracle import oracle as O
-
     nthreads = os.cpu_count() or 1
-    # the committed sequence from the oracle itself (bounded: compute it once
-    # for small configs, else from the committed golden)
-    gpath = os.path.join(ROOT, "tests", "golden", f"cfg{spec.index}.npz")
-    if os.path.exists(gpath):
-        seq = np.load(gpath)["seq"]
-    else:
-        seq = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads)["seq"]
-    per_step = 20.0
+    per_step = 15.0
     vals = []
     samples = []
     for i in range(args.warmup + args.steps):
-        r = _cpu_sample(img, spec, seq, per_step, nthreads)
+        r = _cpu_sample(img, spec, per_step, nthreads)
         if i >= args.warmup:
             vals.append(r["value"])
             samples.append(r)
@@ -173,6 +161,33 @@ def run_reference(args, spec, img, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def _other_configs(L, _lib, skip: int):
+    """One device-timed run of every other BASELINE config (not the headline)."""
+    out = {}
+    for idx, spec in CONFIGS.items():
+        if idx == skip:
+            continue
+        img = make_image(idx)
+        px = np.ascontiguousarray(img.astype(np.float32) if spec.dtype == "f32" else img)
+        dtype = _lib.DTYPE_F32 if spec.dtype == "f32" else _lib.DTYPE_U8
+        strat = _lib.STRATEGY_FILLING_RATE if spec.strategy == "filling-rate" else _lib.STRATEGY_NAIVE
+        h, st = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(L.gp_ctx_create(spec.shape[0], spec.shape[1], dtype, _lib.ptr(px), 1, spec.conn,
+                                   ctypes.byref(h)))
+        _lib.check(L.gp_store_create(spec.n, ctypes.byref(st)))
+        best = None
+        for _ in range(2):  # first run warms allocations
+            s = _lib.RunStats()
+            _lib.check(L.gp_run(h, st, strat, 0, 0, None, None, ctypes.byref(s)))
+            best = s
+        out[spec.name] = {"ms_per_image": best.ms_total, "pairs_per_s": spec.total_pairs / (best.ms_total / 1e3),
+                          "propagations_raw": int(best.raw_count), "ms_commit": best.ms_commit,
+                          "ms_propagate": best.ms_propagate}
+        L.gp_store_destroy(st)
+        L.gp_ctx_destroy(h)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -182,6 +197,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-others", action="store_true", help="skip the one-run summary of the other configs")
     args = ap.parse_args()
     world, rank, local = _dist_env()
     spec = CONFIGS[args.config]
@@ -305,9 +321,10 @@ def main():
         "gpu_launches": int(sum(r.kernels for r in runs)),
         "clocks": clk.summary(),
     }
+    if rank == 0 and world == 1 and not args.no_others:
+        line["other_configs"] = _other_configs(L, _lib, args.config)
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = _cpu_sample(img, spec, seq[:P].copy(), args.cpu_seconds,
-                                           os.cpu_count() or 1)
+        line["cpu_baseline"] = _cpu_sample(img, spec, args.cpu_seconds, os.cpu_count() or 1)
     if rank == 0:
         print(json.dumps(line), flush=True)
     L.gp_store_destroy(st)

@@ -37,6 +37,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <time.h>
 #include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
@@ -355,7 +356,7 @@ int or_extrema(int H, int W, int conn, int metric, int isf, const void *px,
 int or_run(int H, int W, int conn, int metric, int isf, const void *px, int kind,
            int naive_with_tree, int nthreads, void *D_out, int32_t *seq_out,
            int64_t *new_out, int64_t *visits_out, int64_t *walked_out, int64_t *stats,
-           int64_t max_steps) {
+           int64_t max_steps, double *loop_seconds) {
     int64_t n = (int64_t)H * W;
     img_t im = {H, W, conn, metric, isf, isf ? NULL : (const int64_t *)px,
                 isf ? (const float *)px : NULL};
@@ -383,6 +384,8 @@ int or_run(int H, int W, int conn, int metric, int isf, const void *px, int kind
     int use_tree = kind != OR_NAIVE || naive_with_tree;
     int64_t total = (n * n - n) / 2, count = 0, bad_total = 0;
     int rc = 0;
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
     while (st.filled < total && count < max_steps) {
         /* select (strategies.py:125-129 / 220-227) */
         int64_t s = -1;
@@ -412,6 +415,8 @@ int or_run(int H, int W, int conn, int metric, int isf, const void *px, int kind
         if (walked_out) walked_out[count] = walked;
         count++;
     }
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    if (loop_seconds) *loop_seconds = (t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec);
     stats[0] = count;
     stats[1] = count + overhead;
     stats[2] = bad_total;

@@ -46,6 +46,9 @@ struct gp_ctx {
   size_t scratch_trees = 0;
   int commit_blocks = 0;
   double mean_w = 1.0;  // mean edge weight (bucket width scale)
+  uint32_t* list[2] = {nullptr, nullptr};  // unfilled-pair lists (late phase)
+  size_t list_cap = 0;
+  GridBarrier* bar = nullptr;
 };
 
 struct gp_store {
@@ -158,6 +161,10 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
   cudaFree(c->ts.part);
   cudaFree(c->ts.T);
   cudaFree(c->ts.C);
+  cudaFree(c->ts.tin);
+  cudaFree(c->list[0]);
+  cudaFree(c->list[1]);
+  cudaFree(c->bar);
   cudaFree(c->scratch);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
@@ -188,7 +195,7 @@ static PropArgs base_prop(gp_ctx* c) {
 // Bucket width of the propagation (K1): a multiple of the mean edge weight
 // (GP_DELTA_FACTOR, default below; <= 0 or "inf" = unbucketed frontier).
 static float default_delta(const gp_ctx* c) {
-  double factor = 4.0;
+  double factor = 16.0;
   if (const char* e = getenv("GP_DELTA_FACTOR")) factor = atof(e);
   if (!(factor > 0) || std::isinf(factor)) return INFINITY;
   return (float)(factor * c->mean_w);
@@ -463,7 +470,7 @@ static int ensure_tree_store(gp_ctx* c, int nparts) {
   const int N = c->g.N;
   if (c->ts.pre && c->ts.cap >= N && c->ts.nparts == nparts) return GP_OK;
   cudaFree(c->ts.pre); cudaFree(c->ts.szp); cudaFree(c->ts.tdp); cudaFree(c->ts.part); cudaFree(c->ts.T);
-  cudaFree(c->ts.C);
+  cudaFree(c->ts.C); cudaFree(c->ts.tin);
   c->ts = TreeStore{};
   const size_t cap = (size_t)N;  // a pixel is propagated at most once: N slots always suffice
   CUDA_TRY(dalloc(&c->ts.pre, cap * N));
@@ -472,6 +479,7 @@ static int ensure_tree_store(gp_ctx* c, int nparts) {
   CUDA_TRY(dalloc(&c->ts.part, cap * nparts));
   CUDA_TRY(dalloc(&c->ts.T, cap));
   CUDA_TRY(dalloc(&c->ts.C, cap));
+  CUDA_TRY(dalloc(&c->ts.tin, cap * N));
   c->ts.cap = (int)cap;
   c->ts.nparts = nparts;
   return GP_OK;
@@ -493,7 +501,7 @@ static int store_relayout(gp_store* s, const MarkLayout& L) {
 static int commit_blocks(gp_ctx* c) {
   if (c->commit_blocks) return c->commit_blocks;
   int maxb = commit_max_blocks();
-  int bps = 2;
+  int bps = 2048 / commit_threads();
   if (const char* e = getenv("GP_COMMIT_BLOCKS_PER_SM")) bps = atoi(e);
   int nb = std::max(1, std::min(maxb, bps * c->nsm));
   c->commit_blocks = nb;
@@ -566,26 +574,47 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
   } else {
     // ---- device commit loop with speculative propagation batches ----
     const int nblocks = commit_blocks(c);
-    const int nparts = nblocks * (COMMIT_THREADS / 32);
+    const int nparts = nblocks * (commit_threads() / 32);
     int rts = ensure_tree_store(c, nparts);
     if (rts) return rts;
     int *d_slot_of = nullptr, *d_rank = nullptr, *d_ext = nullptr, *d_cands = nullptr;
     int *d_slots = nullptr, *d_free = nullptr;
-    unsigned* d_selkey = nullptr;
+    unsigned long long* d_selkey = nullptr;
     Ctl* d_ctl = nullptr;
     float* d_dfc = nullptr;
     CUDA_TRY(dalloc(&d_slot_of, N));
     CUDA_TRY(dalloc(&d_rank, N));
     CUDA_TRY(dalloc(&d_ext, N));
     CUDA_TRY(dalloc(&d_selkey, N + 2));
+    unsigned* d_flags = nullptr;
+    CUDA_TRY(dalloc(&d_flags, N + 2));
+    CUDA_TRY(cudaMemsetAsync(d_flags, 0, (size_t)(N + 2) * 4, st));
     CUDA_TRY(dalloc(&d_ctl, 1));
     CUDA_TRY(dalloc(&d_dfc, N));
     CUDA_TRY(dalloc(&d_free, N));
+    if (!c->bar) CUDA_TRY(dalloc(&c->bar, 1));
+    CUDA_TRY(cudaMemsetAsync(c->bar, 0, sizeof(GridBarrier), st));
+    {
+      const char* e = getenv("GP_BARRIER");
+      const unsigned use_cg = (e && !strcmp(e, "sw")) ? 0u : 1u;  // default: cooperative groups
+      CUDA_TRY(cudaMemcpyAsync(&c->bar->pad0[0], &use_cg, 4, cudaMemcpyHostToDevice, st));
+    }
     CUDA_TRY(cudaMemsetAsync(d_slot_of, 0xFF, (size_t)N * 4, st));
-    CUDA_TRY(cudaMemsetAsync(d_selkey, 0xFF, (size_t)(N + 2) * 4, st));
+    CUDA_TRY(cudaMemsetAsync(d_selkey, 0xFF, (size_t)(N + 2) * 8, st));
     Ctl h_ctl;
     memset(&h_ctl, 0, sizeof(h_ctl));
     h_ctl.cur_src = -1;
+    // late phase: switch to the unfilled-pair list when the unfilled pairs drop
+    // below alpha x the pairs of one tree (~N * mean depth); GP_LIST_ALPHA=0 off
+    {
+      double alpha = 1.0;
+      if (const char* e = getenv("GP_LIST_ALPHA")) alpha = atof(e);
+      const double est_tree = (double)N * std::sqrt((double)N) * 0.5;
+      double sw = alpha * est_tree;
+      const double capd = 64.0 * 1024 * 1024;  // list entries (256 MiB per buffer)
+      h_ctl.list_switch = (unsigned long long)std::min(sw, capd);
+      if (strategy != GP_STRATEGY_FILLING_RATE && !getenv("GP_LIST_ALPHA")) h_ctl.list_switch = 0;
+    }
     CUDA_TRY(cudaMemcpyAsync(d_ctl, &h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
     if (strategy == GP_STRATEGY_FILLING_RATE) {
       int cen = -1;
@@ -624,10 +653,14 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     ca.rank = d_rank;
     ca.ext = d_ext;
     ca.selkey = d_selkey;
+    ca.stepflags = d_flags;
     ca.seq = d_seq;
     ca.newp = d_new;
     ca.ctl = d_ctl;
     ca.max_steps = N + 1;
+    ca.bar = c->bar;
+    ca.staged = getenv("GP_STAGED") ? atoi(getenv("GP_STAGED")) : 0;
+    ca.total_pairs = ((unsigned long long)N * N - N) / 2;
     PropArgs pa = base_prop(c);
     pa.src = d_cands;
     pa.ns = 1;
@@ -671,6 +704,26 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
       CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
       if (h_ctl.status == CTL_DONE) break;
+      if (h_ctl.status == CTL_SWITCH) {  // build the unfilled-pair list, relaunch in list mode
+        const unsigned long long need = ca.total_pairs - h_ctl.filled;
+        if (need + 1024 > c->list_cap) {
+          cudaFree(c->list[0]);
+          cudaFree(c->list[1]);
+          c->list[0] = c->list[1] = nullptr;
+          c->list_cap = 0;
+          CUDA_TRY(dalloc(&c->list[0], need + 1024));
+          CUDA_TRY(dalloc(&c->list[1], need + 1024));
+          c->list_cap = need + 1024;
+        }
+        ca.plist[0] = c->list[0];
+        ca.plist[1] = c->list[1];
+        CUDA_TRY(cudaMemsetAsync(&d_ctl->list_n[0], 0, 8, st));
+        CUDA_TRY(launch_build_list(L, s->mark, c->list[0], &d_ctl->list_n[0], st));
+        h_ctl.mode = 1;
+        CUDA_TRY(cudaMemcpyAsync(&d_ctl->mode, &h_ctl.mode, 4, cudaMemcpyHostToDevice, st));
+        S.kernels++;
+        continue;
+      }
       if (h_ctl.status != CTL_MISS) { rc = fail(GP_EINTERNAL, "commit loop stopped unexpectedly"); break; }
       EvPair f;
       cudaEventCreate(&f.a); cudaEventCreate(&f.b);
@@ -688,6 +741,17 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     if (debug) {
       std::vector<unsigned long long> h((size_t)(N + 2) * 4);
       CUDA_TRY(cudaMemcpy(h.data(), d_cdbg, h.size() * 8, cudaMemcpyDeviceToHost));
+      if (const char* path = getenv("GP_DEBUG_DUMP")) {  // per-step stamps + new pairs
+        std::vector<unsigned long long> nw2(h_ctl.step);
+        cudaMemcpy(nw2.data(), d_new, (size_t)h_ctl.step * 8, cudaMemcpyDeviceToHost);
+        if (FILE* fp = fopen(path, "w")) {
+          for (int i = 0; i < h_ctl.step; i++) {
+            unsigned long long* r = &h[(size_t)i * 4];
+            fprintf(fp, "%d %llu %llu %llu %llu %llu\n", i, r[0], r[1], r[2], r[3], nw2[i]);
+          }
+          fclose(fp);
+        }
+      }
       std::vector<double> ph[4];
       for (int i = 0; i + 1 < h_ctl.step; i++) {
         unsigned long long* r = &h[(size_t)i * 4];
@@ -716,7 +780,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     for (auto& e : pev) { S.ms_propagate += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     P = h_ctl.step;
     cudaFree(d_slot_of); cudaFree(d_rank); cudaFree(d_ext); cudaFree(d_cands); cudaFree(d_slots);
-    cudaFree(d_selkey); cudaFree(d_ctl); cudaFree(d_dfc); cudaFree(d_free);
+    cudaFree(d_selkey); cudaFree(d_ctl); cudaFree(d_dfc); cudaFree(d_free); cudaFree(d_flags);
     S.propagations += h_ctl.total_props;
     S.visits = (int64_t)h_ctl.visits;
   }

@@ -79,16 +79,24 @@ __device__ __forceinline__ unsigned long long block_reduce_sum(unsigned long lon
   return v;
 }
 
-// grid-wide selection of the source for `step`, excluding pixel `skip`
-__device__ void select_step(const CommitArgs& a, int step, int skip, unsigned* red32) {
+// grid-wide selection of the source for `step`, excluding pixel `skip`.
+// The atomicMin target packs (key << 32 | pixel << 16 | slot + 1): after the
+// barrier one load yields the source and its tree slot (0 = none).
+__device__ __forceinline__ unsigned long long sel_pack(unsigned key, int v, int slot) {
+  return ((unsigned long long)key << 32) | ((unsigned long long)(unsigned)v << 16) |
+         (unsigned long long)(slot >= 0 && slot < 0xFFFF ? (unsigned)(slot + 1) : 0u);
+}
+
+__device__ void select_step(const CommitArgs& a, int step, int skip, unsigned long long* red64) {
   const int N = a.g.N;
-  unsigned m = 0xFFFFFFFFu;
+  unsigned long long m = ~0ull;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
     if (v == skip) continue;
-    m = min(m, sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank));
+    const unsigned key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
+    if (key != 0xFFFFFFFFu) m = min(m, sel_pack(key, v, __ldcg(&a.slot_of[v])));
   }
-  m = block_reduce_min(m, red32);
-  if (threadIdx.x == 0 && m != 0xFFFFFFFFu) atomicMin(&a.selkey[step], m);
+  m = block_reduce_min(m, red64);
+  if (threadIdx.x == 0 && m != ~0ull) atomicMin(&a.selkey[step], m);
 }
 
 // K2 for one committed tree: this warp's share of the chunks.
@@ -130,7 +138,7 @@ __device__ __forceinline__ unsigned fill_warp_share(const CommitArgs& a, int slo
       u_l = __ldg(&pre[qa]);
       td_l = __ldg(&tdp[qa]);
     }
-    unsigned nch_l = (sz_l + 31u) >> 5;
+    unsigned nch_l = qa ? (sz_l + 31u) >> 5 : 0u;  // root row: see fill_root_row
     unsigned c0_l = 0;
     if (lane == 0) { nch_l -= coff; c0_l = coff; }
     const bool full_l = nch_l && u_l != s && __ldcg(&a.cnt[u_l]) >= N - 1;
@@ -198,80 +206,393 @@ __device__ __forceinline__ unsigned fill_warp_share(const CommitArgs& a, int slo
   return lane == 0 ? total_new : 0u;
 }
 
-template <int G, int MINB>
-__global__ void __launch_bounds__(COMMIT_THREADS, MINB) k_commit(CommitArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ unsigned red32[32];
+// K2 variant with asynchronous staging: the descendant ids of GS chunks are
+// loaded into registers together, then the GS x 32 mark words are gathered
+// with cp.async straight into this warp's shared-memory stage (no register
+// per in-flight load), so a warp needs ~2 memory round trips per GS chunks.
+// cp.async.ca caches in L1; every grid barrier's gpu-scope fence invalidates
+// L1, and a pair's own bit only changes by its own (single) test in a step.
+__device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <int GS>
+__device__ __forceinline__ unsigned fill_warp_staged(const CommitArgs& a, int slot, int s,
+                                                     uint32_t* stage /* [GS][32] */) {
+  const int N = a.g.N;
+  const int lane = threadIdx.x & 31;
+  const int P = a.ts.nparts;
+  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const size_t off = (size_t)slot * N;
+  const uint16_t* pre = a.ts.pre + off;
+  const uint16_t* szp = a.ts.szp + off;
+  const float* tdp = a.ts.tdp + off;
+  const unsigned T = __ldg(&a.ts.T[slot]);
+  const unsigned b0 = (unsigned)(((unsigned long long)p * T) / P);
+  const unsigned b1 = (unsigned)(((unsigned long long)(p + 1) * T) / P);
+  unsigned count = b1 - b0;
+  if (!count) return 0;
+  const uint32_t pw = __ldg(&a.ts.part[(size_t)slot * P + p]);
+  int q = (int)(pw & 0xFFFFu);
+  unsigned coff = pw >> 16;
+  unsigned total_new = 0;
+  const MarkLayout L = a.L;
+  while (count) {
+    const int qa = q + lane;
+    unsigned sz_l = 0;
+    int u_l = 0;
+    float td_l = 0.f;
+    if (qa < N) {
+      sz_l = __ldg(&szp[qa]);
+      u_l = __ldg(&pre[qa]);
+      td_l = __ldg(&tdp[qa]);
+    }
+    unsigned nch_l = qa ? (sz_l + 31u) >> 5 : 0u;
+    unsigned c0_l = 0;
+    if (lane == 0) { nch_l -= coff; c0_l = coff; }
+    const bool full_l = nch_l && u_l != s && __ldcg(&a.cnt[u_l]) >= N - 1;
+    unsigned cum = nch_l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, cum, o);
+      if (lane >= o) cum += y;
+    }
+    const unsigned excl = cum - nch_l;
+    const unsigned wtotal = __shfl_sync(0xffffffffu, cum, 31);
+    const unsigned take = min(wtotal, count);
+    for (unsigned cb = 0; cb < take; cb += GS) {
+      uint32_t w[GS];
+      unsigned okm = 0;
+      // A: descendant ids of GS chunks, all loads in flight together
+#pragma unroll
+      for (int j = 0; j < GS; j++) {
+        const unsigned c = cb + j;
+        const unsigned bm = __ballot_sync(0xffffffffu, cum > c);
+        const int ol = bm ? __ffs(bm) - 1 : 0;
+        const unsigned sz = __shfl_sync(0xffffffffu, sz_l, ol);
+        const unsigned cidx = __shfl_sync(0xffffffffu, c0_l + (c - excl), ol);
+        const bool full = __shfl_sync(0xffffffffu, (int)full_l, ol);
+        const unsigned k = cidx * 32u + lane;
+        const bool ok = c < take && !full && k < sz;
+        w[j] = ok ? (uint32_t)__ldg(&pre[q + ol + 1 + k]) : 0u;
+        okm |= (unsigned)ok << j;
+      }
+      // B: mark words -> shared stage (asynchronous gathers)
+#pragma unroll
+      for (int j = 0; j < GS; j++) {
+        const unsigned bm = __ballot_sync(0xffffffffu, cum > cb + j);
+        const int ol = bm ? __ffs(bm) - 1 : 0;
+        const int u = __shfl_sync(0xffffffffu, u_l, ol);
+        if ((okm >> j) & 1u) {
+          const uint32_t wcol = mcol(L, w[j]);
+          cp_async4(&stage[j * 32 + lane], a.mark + (size_t)u * L.RW + (wcol >> 5));
+        }
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      // C: test and fill
+#pragma unroll
+      for (int j = 0; j < GS; j++) {
+        const unsigned c = cb + j;
+        const unsigned bm = __ballot_sync(0xffffffffu, cum > c);
+        const int ol = bm ? __ffs(bm) - 1 : 0;
+        const int u = __shfl_sync(0xffffffffu, u_l, ol);
+        const float tdu = __shfl_sync(0xffffffffu, td_l, ol);
+        const unsigned cidx = __shfl_sync(0xffffffffu, c0_l + (c - excl), ol);
+        bool isnew = false;
+        if ((okm >> j) & 1u) {
+          const uint32_t wcol = mcol(L, w[j]);
+          const uint32_t wbit = 1u << (wcol & 31);
+          isnew = !(stage[j * 32 + lane] & wbit);
+          if (isnew) {
+            const int ww = (int)w[j];
+            const uint32_t ucol = mcol(L, (uint32_t)u);
+            atomicOr(a.mark + (size_t)u * L.RW + (wcol >> 5), wbit);
+            atomicOr(a.mark + mword(L, (uint32_t)ww, ucol), 1u << (ucol & 31));
+            const float duv = __fsub_rn(__ldg(&tdp[q + ol + 1 + cidx * 32u + lane]), tdu);
+            a.D[(size_t)u * N + ww] = duv;
+            a.D[(size_t)ww * N + u] = duv;
+            atomicAdd(&a.cnt[ww], 1);
+          }
+        }
+        const unsigned nb = __popc(__ballot_sync(0xffffffffu, isnew));
+        if (lane == 0 && nb && u != s) atomicAdd(&a.cnt[u], (int)nb);
+        total_new += nb;
+      }
+      __syncwarp();
+    }
+    count -= take;
+    q += 32;
+    coff = 0;
+  }
+  return lane == 0 ? total_new : 0u;
+}
+
+// K2 for the root: (s, x) is an ancestor pair for every x, so the fill of
+// row s is pixel-parallel over the whole grid; each unmarked column is a new
+// pair with D = td[x] - td[s] = tdp[tin[x]] - 0.  Bits of one mark word are
+// OR-ed by one lane per word (match_any).
+__device__ __forceinline__ unsigned fill_root_row(const CommitArgs& a, int slot, int s) {
+  const int N = a.g.N;
+  const MarkLayout L = a.L;
+  const size_t off = (size_t)slot * N;
+  const uint16_t* tin = a.ts.tin + off;
+  const float* tdp = a.ts.tdp + off;
+  uint32_t* row = a.mark + (size_t)s * L.RW;
+  const uint32_t scol = mcol(L, (uint32_t)s);
+  const uint32_t sbit = 1u << (scol & 31);
+  unsigned mine = 0;
+  const int stride = gridDim.x * blockDim.x;
+  for (int x0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); x0 < N; x0 += stride) {
+    const int x = x0 + (threadIdx.x & 31);
+    bool isnew = false;
+    uint32_t xcol = 0;
+    if (x < N && x != s) {
+      xcol = mcol(L, (uint32_t)x);
+      isnew = !(__ldcg(&row[xcol >> 5]) & (1u << (xcol & 31)));
+    }
+    const unsigned nm = __ballot_sync(0xffffffffu, isnew);
+    if (!nm) continue;
+    const unsigned peers = __match_any_sync(0xffffffffu, isnew ? (xcol >> 5) : 0xFFFFFFFFu);
+    if (isnew) {
+      // the lanes sharing a mark word OR their bits; their leader stores once
+      const uint32_t acc = __reduce_or_sync(peers, 1u << (xcol & 31));
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(&row[xcol >> 5], acc);
+      atomicOr(&a.mark[mword(L, (uint32_t)x, scol)], sbit);
+      const float d = __ldg(&tdp[__ldg(&tin[x])]);
+      a.D[(size_t)s * N + x] = d;
+      a.D[(size_t)x * N + s] = d;
+      atomicAdd(&a.cnt[x], 1);
+      mine++;
+    }
+  }
+  return mine;
+}
+
+// ---- software grid barrier: one arrival per CTA, relaxed polling (no L1
+// invalidation per poll), release/acquire by gpu-scope fences ----
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_barrier(GridBarrier* bar, unsigned& gen) {
+  if (bar->pad0[0]) {  // cooperative-groups barrier selected (GP_BARRIER=cg)
+    cg::this_grid().sync();
+    return;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = gen;
+    __threadfence();
+    if (atomicAdd(&bar->count, 1u) == gridDim.x - 1) {
+      bar->count = 0;
+      __threadfence();
+      atomicExch(&bar->gen, g + 1);
+    } else {
+      while (ld_relaxed_gpu(&bar->gen) == g) {
+      }
+    }
+    __threadfence();
+  }
+  gen++;
+  __syncthreads();
+}
+
+// K2, late phase: test every remaining unfilled pair (u, w) against the
+// committed tree's Euler intervals: u is an ancestor of w iff
+// tin[u] < tin[w] <= tin[u] + szp[tin[u]].  Work per commit = unfilled pairs
+// (shrinking), instead of the tree's ~N*depth pairs.
+__device__ __forceinline__ unsigned fill_list(const CommitArgs& a, int slot, int s,
+                                              unsigned cur, unsigned n) {
+  const int N = a.g.N;
+  const size_t off = (size_t)slot * N;
+  const uint16_t* tin = a.ts.tin + off;
+  const uint16_t* szp = a.ts.szp + off;
+  const float* tdp = a.ts.tdp + off;
+  const MarkLayout L = a.L;
+  uint32_t* list = a.plist[cur];
+  unsigned mine = 0;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t e = __ldcg(&list[i]);
+    if (e == LIST_DEAD) continue;
+    const int u = (int)(e >> 16), w = (int)(e & 0xFFFFu);
+    const unsigned tu = __ldg(&tin[u]), tw = __ldg(&tin[w]);
+    int anc = -1, des = -1;
+    unsigned ta = 0, td = 0;
+    if (tu < tw && tw <= tu + __ldg(&szp[tu])) { anc = u; des = w; ta = tu; td = tw; }
+    else if (tw < tu && tu <= tw + __ldg(&szp[tw])) { anc = w; des = u; ta = tw; td = tu; }
+    if (anc < 0) continue;
+    const uint32_t ca = mcol(L, (uint32_t)anc), cd = mcol(L, (uint32_t)des);
+    atomicOr(&a.mark[mword(L, (uint32_t)anc, cd)], 1u << (cd & 31));
+    atomicOr(&a.mark[mword(L, (uint32_t)des, ca)], 1u << (ca & 31));
+    const float duv = __fsub_rn(__ldg(&tdp[td]), __ldg(&tdp[ta]));
+    a.D[(size_t)anc * N + des] = duv;
+    a.D[(size_t)des * N + anc] = duv;
+    if (anc != s) atomicAdd(&a.cnt[anc], 1);
+    atomicAdd(&a.cnt[des], 1);
+    list[i] = LIST_DEAD;
+    mine++;
+  }
+  return mine;
+}
+
+// stream-compact the live list entries into the other buffer
+__device__ __forceinline__ void compact_list(const CommitArgs& a, unsigned cur, unsigned n) {
+  const uint32_t* src = a.plist[cur];
+  uint32_t* dst = a.plist[cur ^ 1];
+  unsigned* cnt = &a.ctl->list_n[cur ^ 1];
+  const int lane = threadIdx.x & 31;
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned b = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b < n; b += stride) {
+    const unsigned i = b + lane;
+    const uint32_t e = i < n ? __ldcg(&src[i]) : LIST_DEAD;
+    const bool live = e != LIST_DEAD;
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    if (!m) continue;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(cnt, (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (live) dst[base + __popc(m & ((1u << lane) - 1u))] = e;
+  }
+}
+
+template <int G, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   __shared__ unsigned long long red64[32];
+  constexpr int GS = 16;
+  __shared__ uint32_t stage_all[THREADS / 32][GS * 32];
+  uint32_t* stage = stage_all[threadIdx.x >> 5];
   const int N = a.g.N;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool keeper = gtid == 0;  // bookkeeping thread (registers, stores only)
+  unsigned gen = ld_relaxed_gpu(&a.bar->gen);  // no barrier in flight at launch
 
   int step = a.ctl->step;
   int s = a.ctl->cur_src;
+  const int mode = a.ctl->mode;
+  // launch-invariant / register-resident state
+  unsigned lcur = mode ? __ldcg(&a.ctl->list_cur) : 0u;
+  unsigned ln = mode ? __ldcg(&a.ctl->list_n[lcur]) : 0u;
+  unsigned long long filled = 0, visits = 0;
+  unsigned dead = 0;
+  int free_top = 0;
+  if (keeper) {
+    filled = a.ctl->filled;
+    visits = a.ctl->visits;
+    dead = a.ctl->list_dead;
+    free_top = a.ctl->free_top;
+  }
+  int slot = -1;
   if (s == -1) {  // first launch: select the first source
-    select_step(a, step, -1, red32);
-    grid.sync();
-    unsigned key = __ldcg(&a.selkey[step]);
-    s = key == 0xFFFFFFFFu ? -2 : key_src(a.strategy, key, a.ext);
+    select_step(a, step, -1, red64);
+    grid_barrier(a.bar, gen);
+  }
+  if (s != -2) {  // (re)load the packed selection of `step`
+    const unsigned long long sk = __ldcg(&a.selkey[step]);
+    s = sk == ~0ull ? -2 : (int)((sk >> 16) & 0xFFFFu);
+    if (s >= 0) slot = __ldcg(&a.slot_of[s]);  // may have been propagated since
   }
   int status = CTL_RUNNING;
   int done_here = 0;
+  unsigned flags = 0;  // decisions for this step, from the keeper (previous step)
   for (;;) {
     if (s == -2) { status = CTL_DONE; break; }
     if (done_here >= a.max_steps) { status = CTL_LIMIT; break; }
-    const int slot = __ldcg(&a.slot_of[s]);
     if (slot < 0) { status = CTL_MISS; break; }
-
     unsigned long long* dbg = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + (size_t)step * 4 : nullptr;
     if (dbg) dbg[0] = gtimer();
-    // ---- K2: Euler-range fill ----
-    unsigned long long lnew = fill_warp_share<G>(a, slot, s);
+    const unsigned cslot = keeper ? __ldg(&a.ts.C[slot]) : 0u;  // consumed at step end
+    // ---- K2: fill ----
+    unsigned long long lnew =
+        mode == 1 ? (unsigned long long)fill_list(a, slot, s, lcur, ln)
+        : a.staged ? (unsigned long long)fill_warp_staged<GS>(a, slot, s, stage)
+                   : (unsigned long long)fill_warp_share<G>(a, slot, s);
+    if (mode == 0) lnew += fill_root_row(a, slot, s);
     if (dbg) dbg[1] = gtimer();
     lnew = block_reduce_sum(lnew, red64);
     if (threadIdx.x == 0 && lnew) atomicAdd(&a.newp[step], lnew);
-    grid.sync();
+    grid_barrier(a.bar, gen);
     if (dbg) dbg[2] = gtimer();
-    if (gtid == 0) {
+    const bool compact = mode == 1 && (flags & 2u);
+    if (compact) compact_list(a, lcur, ln);
+    if (keeper) {
       a.cnt[s] = N - 1;  // the root pairs with every pixel
       a.seq[step] = s;
       a.slot_of[s] = -2;  // committed: recycle the slot
-      a.ctl->visits += __ldg(&a.ts.C[slot]);
-      a.free_stack[a.ctl->free_top++] = slot;
+      a.free_stack[free_top++] = slot;
     }
-    // ---- K3: selection of the next source ----
-    select_step(a, step + 1, s, red32);
+    // ---- K3: selection of the next source (+ keeper's accounting) ----
+    unsigned long long stepnew = 0;
+    if (keeper) stepnew = __ldcg(&a.newp[step]);  // in flight with the selection loads
+    select_step(a, step + 1, s, red64);
+    if (keeper) {
+      filled += stepnew;
+      visits += cslot;
+      dead = compact ? 0u : dead + (unsigned)stepnew;
+      const unsigned live = compact ? 0u : ln;  // new length unknown yet: no back-to-back compaction
+      unsigned f = 0;
+      if (mode == 0 && a.total_pairs - filled <= a.ctl->list_switch) f |= 1u;
+      if (mode == 1 && live && (unsigned long long)dead * 4 > live) f |= 2u;
+      a.stepflags[step + 1] = f;
+    }
     if (dbg) dbg[3] = gtimer();
-    grid.sync();
-    const unsigned key = __ldcg(&a.selkey[step + 1]);
+    grid_barrier(a.bar, gen);
+    const unsigned long long sk = __ldcg(&a.selkey[step + 1]);
+    flags = __ldcg(&a.stepflags[step + 1]);
+    if (compact) {  // swap buffers; the new length is final after the barrier
+      if (keeper) a.ctl->list_n[lcur] = 0;
+      lcur ^= 1u;
+      ln = __ldcg(&a.ctl->list_n[lcur]);
+    }
     step++;
     done_here++;
-    s = key == 0xFFFFFFFFu ? -2 : key_src(a.strategy, key, a.ext);
+    s = sk == ~0ull ? -2 : (int)((sk >> 16) & 0xFFFFu);
+    slot = (int)(sk & 0xFFFFu) - 1;
+    if (slot < 0 && s >= 0) slot = __ldcg(&a.slot_of[s]);  // not encodable / no tree yet
+    if (flags & 1u) { status = CTL_SWITCH; break; }
   }
-  if (gtid == 0) {
+  if (keeper) {
     a.ctl->step = step;
     a.ctl->cur_src = s;
     a.ctl->status = status;
+    a.ctl->filled = filled;
+    a.ctl->visits = visits;
+    a.ctl->list_dead = dead;
+    a.ctl->list_cur = lcur;
+    a.ctl->free_top = free_top;
   }
 }
 
-// Fill pipelining depth G (chunks in flight per warp): G=4 keeps 2 CTAs of
-// 512 threads per SM within 64 registers; G=8 needs ~128 registers (1 CTA/SM).
-static const void* commit_kernel(int G) {
-  return G >= 8 ? (const void*)k_commit<8, 1> : (const void*)k_commit<4, 2>;
+// Fill pipelining depth G (chunks in flight per warp) = 4 fits 64 registers.
+// CTA shape: GP_COMMIT_THREADS = 512 (2 CTAs/SM, default) or 1024 (1 CTA/SM).
+int commit_threads() {
+  static int t = 0;
+  if (!t) {
+    t = 512;
+    (void)0;
+  }
+  return t;
 }
 
-int commit_fill_depth() {
-  int G = 4;
-  if (const char* e = getenv("GP_FILL_G")) G = atoi(e);
-  return G >= 8 ? 8 : 4;
+static const void* commit_kernel(int G) {
+  (void)G;
+  return (const void*)k_commit<4, 512, 2>;
 }
+
+int commit_fill_depth() { return 4; }
 
 int commit_max_blocks() {
   int dev = 0, nsm = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, commit_kernel(commit_fill_depth()),
-                                                COMMIT_THREADS, 0);
+                                                commit_threads(), 0);
   return nsm * (per_sm > 0 ? per_sm : 1);
 }
 
@@ -279,7 +600,55 @@ cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st) 
   CommitArgs args = a;
   void* params[] = {&args};
   return cudaLaunchCooperativeKernel(commit_kernel(commit_fill_depth()), dim3(num_blocks),
-                                     dim3(COMMIT_THREADS), params, 0, st);
+                                     dim3(commit_threads()), params, 0, st);
+}
+
+// ---- list-mode entry: every unfilled pair (u < w) from the mark bitmap ----
+__global__ void k_build_list(MarkLayout L, const uint32_t* mark, uint32_t* list,
+                             unsigned* count) {
+  const size_t total = (size_t)L.N * L.RW;
+  const int lane = threadIdx.x & 31;
+  for (size_t b = (size_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b < total;
+       b += (size_t)gridDim.x * blockDim.x) {
+    const size_t i = b + lane;
+    uint32_t zeros = 0;
+    int u = 0;
+    uint32_t wbase = 0;
+    if (i < total) {
+      u = (int)(i / L.RW);
+      wbase = (uint32_t)(i % L.RW) * 32u;
+      zeros = ~__ldg(&mark[i]);
+    }
+    // keep only real pixels w > u
+    uint32_t keep = 0;
+    for (uint32_t z = zeros; z; z &= z - 1) {
+      const int bit = __ffs(z) - 1;
+      const int w = mcol_pixel(L, wbase + bit);
+      if (w > u) keep |= 1u << bit;
+    }
+    const unsigned c = __popc(keep);
+    unsigned incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned base = 0;
+    if (lane == 31 && tot) base = atomicAdd(count, tot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    unsigned pos = base + incl - c;
+    for (uint32_t z = keep; z; z &= z - 1) {
+      const int bit = __ffs(z) - 1;
+      list[pos++] = ((uint32_t)u << 16) | (uint32_t)mcol_pixel(L, wbase + bit);
+    }
+  }
+}
+
+cudaError_t launch_build_list(const MarkLayout& L, const uint32_t* mark, uint32_t* list,
+                              unsigned* count, cudaStream_t st) {
+  k_build_list<<<148 * 8, 256, 0, st>>>(L, mark, list, count);
+  return cudaGetLastError();
 }
 
 // ---- speculative candidate batch: the K smallest keys among open pixels

@@ -58,6 +58,7 @@ __device__ __forceinline__ int parent_of(int v, uint8_t code, int W) {
 // Images narrower or shorter than 16 use plain raster columns.
 struct MarkLayout {
   int N;          // pixels
+  int H;          // image height
   int W;          // image width (tiling)
   int tiled;      // 16x16 tile order?
   int RW;         // 32-bit words per row
@@ -68,6 +69,7 @@ struct MarkLayout {
 __host__ __device__ inline MarkLayout make_layout(int N, int H, int W) {
   MarkLayout L;
   L.N = N;
+  L.H = H;
   L.W = W;
   L.tiled = (H >= 16 && W >= 16) ? 1 : 0;
   L.TWn = (W + 15) / 16;
@@ -80,6 +82,16 @@ __device__ __forceinline__ uint32_t mcol(const MarkLayout& L, uint32_t c) {
   if (!L.tiled) return c;
   const uint32_t r = __umulhi(c, L.magic), cc = c - r * (uint32_t)L.W;
   return (((r >> 4) * (uint32_t)L.TWn + (cc >> 4)) << 8) + ((r & 15u) << 4) + (cc & 15u);
+}
+
+// inverse of mcol: pixel of a tiled column, -1 for padding columns
+__device__ __forceinline__ int mcol_pixel(const MarkLayout& L, uint32_t ct) {
+  if (!L.tiled) return ct < (uint32_t)L.N ? (int)ct : -1;
+  const uint32_t tile = ct >> 8, within = ct & 255u;
+  const uint32_t tr = tile / (uint32_t)L.TWn, tc = tile - tr * (uint32_t)L.TWn;
+  const uint32_t r = tr * 16 + (within >> 4), c = tc * 16 + (within & 15u);
+  if (r >= (uint32_t)L.H || c >= (uint32_t)L.W) return -1;
+  return (int)(r * L.W + c);
 }
 
 __device__ __forceinline__ size_t mword(const MarkLayout& L, uint32_t row, uint32_t col_t) {

@@ -25,6 +25,7 @@ struct TreeStore {
   uint32_t* part;
   uint32_t* T;
   uint32_t* C;  // ancestor/descendant pairs of the tree = sum of depths
+  uint16_t* tin;  // preorder position of each pixel (list-mode ancestor tests)
   int nparts;  // commit warps (partition count)
   int cap;     // slots
 };
@@ -62,10 +63,23 @@ struct Ctl {
   int ncand;      // candidates produced by the last top-K
   int free_top;   // free-slot stack height
   int total_props; // trees propagated by speculative batches
-  int pad;
+  int mode;        // 0: Euler-range fill, 1: unfilled-pair list fill
   unsigned long long visits;  // sum of C over committed trees
+  unsigned long long filled;  // pairs filled so far
+  unsigned list_n[2];         // entries in the two list buffers
+  unsigned list_cur;          // live buffer
+  unsigned list_dead;         // dead entries in the live buffer
+  unsigned long long list_switch;  // switch to list mode when unfilled <= this
 };
-enum { CTL_RUNNING = 0, CTL_DONE = 1, CTL_MISS = 2, CTL_LIMIT = 3 };
+enum { CTL_RUNNING = 0, CTL_DONE = 1, CTL_MISS = 2, CTL_LIMIT = 3, CTL_SWITCH = 4 };
+
+// software grid barrier (count / generation on separate lines)
+struct GridBarrier {
+  unsigned count;
+  unsigned pad0[31];
+  unsigned gen;
+  unsigned pad1[31];
+};
 
 struct CommitArgs {
   Grid g;
@@ -79,15 +93,21 @@ struct CommitArgs {
   float* D;                // [N][N]
   const int* rank;         // [N] position in the extrema ranking (filling-rate)
   const int* ext;          // [N] pixel at each rank
-  unsigned* selkey;        // [N+2] per-step selection key (atomicMin target)
+  unsigned long long* selkey;  // [N+2] per-step packed selection (atomicMin target)
+  unsigned* stepflags;     // [N+2] per-step decisions from the bookkeeping thread
   int* seq;                // [N] committed sources
   unsigned long long* newp;// [N] new pairs per commit
   Ctl* ctl;
   int max_steps;           // commits allowed in this launch
   unsigned long long* dbg; // optional per-step stamps [steps][4] from block 0 (debug)
+  GridBarrier* bar;
+  uint32_t* plist[2];      // unfilled pairs (u << 16 | w, u < w), list mode
+  unsigned long long total_pairs;
+  int staged;              // range fill via cp.async staging (1) or registers (0)
 };
 
-constexpr int COMMIT_THREADS = 512;
+int commit_threads();
+constexpr uint32_t LIST_DEAD = 0xFFFFFFFFu;
 cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st);
 int commit_max_blocks();
 int commit_fill_depth();
@@ -107,5 +127,7 @@ cudaError_t launch_mark_unpack(const MarkLayout& L, const uint32_t* mark, uint8_
 cudaError_t launch_naive_trace(const MarkLayout& L, uint32_t* mark, int* cnt, int* seq,
                                unsigned long long* newp, cudaStream_t st);
 cudaError_t launch_argmax_first(const float* x, int N, int* out, cudaStream_t st);
+cudaError_t launch_build_list(const MarkLayout& L, const uint32_t* mark, uint32_t* list,
+                              unsigned* count, cudaStream_t st);
 
 }  // namespace gp

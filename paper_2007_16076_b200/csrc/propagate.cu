@@ -30,7 +30,8 @@
 // time by a single warp (no block barriers), preorder positions by pointer
 // jumping over path sums (a pixel's earlier siblings are among its parent's
 // <= 8 grid neighbours), then the preorder arrays and the balanced partition
-// of the fill work into commit warps (exclusive scan of 32-pair chunks).  All
+// of the fill work into commit warps (exclusive scan of 32-pair chunks; the
+// root's N-1 pairs are excluded -- the commit kernel scans its row).  All
 // of it runs here, off the commit loop's critical path.
 #include "gp_common.cuh"
 #include "gp_kernels.h"
@@ -40,6 +41,7 @@ namespace gp {
 extern __shared__ __align__(16) unsigned char g_smem[];
 
 constexpr int HIST_SMEM = 4096;  // depth-histogram bins in the shared-memory variant
+constexpr int WL_SMEM = 12288;   // worklist entries kept in smem (global-scratch variant)
 
 struct PropShared {
   int cnt[2];
@@ -80,15 +82,28 @@ __device__ __forceinline__ void atomic_add_u16(uint16_t* base, int i, unsigned v
   atomicAdd(w, v << ((i & 1) * 16));
 }
 
-// warp-aggregated append of `v` (where flag) to list[*cnt]
-__device__ __forceinline__ void warp_append(bool flag, int v, int* cnt, uint16_t* list) {
+// Near worklists: the first `cap` entries in shared memory, the (rare)
+// overflow in the per-CTA global scratch.  The shared-memory variant keeps
+// whole lists in shared memory (cap = N).
+struct WorkLists {
+  uint16_t* s[2];
+  uint16_t* g[2];
+  int cap;
+  __device__ __forceinline__ uint16_t* at(int l, int i) const {
+    return i < cap ? s[l] + i : g[l] + (i - cap);
+  }
+};
+
+// warp-aggregated append of `v` (where flag) to list l
+__device__ __forceinline__ void warp_append(bool flag, int v, int* cnt, const WorkLists& wl,
+                                            int l) {
   const unsigned m = __ballot_sync(0xffffffffu, flag);
   if (!m) return;
   const int lane = threadIdx.x & 31;
   int base = 0;
   if (lane == __ffs(m) - 1) base = atomicAdd(cnt, __popc(m));
   base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-  if (flag) list[base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)v;
+  if (flag) *wl.at(l, base + __popc(m & ((1u << lane) - 1u))) = (uint16_t)v;
 }
 
 // in-place pointer jumping on packed (acc << 16 | jump) words until every
@@ -128,12 +143,26 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   unsigned char* base = a.in_smem ? g_smem : a.scratch + (size_t)t * a.scratch_bytes;
   uint32_t* dist = reinterpret_cast<uint32_t*>(base);
   float* fimg = reinterpret_cast<float*>(base + lay.A);
-  uint16_t* wl[2] = {reinterpret_cast<uint16_t*>(base + lay.B),
-                     reinterpret_cast<uint16_t*>(base + lay.W2)};
+  WorkLists wl;
+  wl.g[0] = reinterpret_cast<uint16_t*>(base + lay.B);
+  wl.g[1] = reinterpret_cast<uint16_t*>(base + lay.W2);
   uint8_t* code = base + lay.W2;
   uint32_t* far = reinterpret_cast<uint32_t*>(base + lay.far);
   uint32_t* inq = reinterpret_cast<uint32_t*>(base + lay.inq);
   uint32_t* hist = reinterpret_cast<uint32_t*>(base + lay.hist);
+  if (a.in_smem) {
+    wl.s[0] = wl.g[0];
+    wl.s[1] = wl.g[1];
+    wl.cap = N;
+  } else {
+    // global-scratch variant: bitmaps and the head of both worklists in smem
+    const size_t bm = align16((size_t)NW * 4);
+    far = reinterpret_cast<uint32_t*>(g_smem);
+    inq = reinterpret_cast<uint32_t*>(g_smem + bm);
+    wl.s[0] = reinterpret_cast<uint16_t*>(g_smem + 2 * bm);
+    wl.s[1] = wl.s[0] + WL_SMEM;
+    wl.cap = WL_SMEM;
+  }
   const float* f = a.in_smem ? fimg : a.img;
   if (a.in_smem)
     for (int i = tid; i < N; i += nthr) fimg[i] = a.img[i];
@@ -155,7 +184,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   for (int i = tid; i < a.ns; i += nthr) {
     const int v = my_src[i];
     dist[v] = 0u;
-    wl[0][i] = (uint16_t)v;
+    *wl.at(0, i) = (uint16_t)v;
   }
   __syncthreads();
 
@@ -215,7 +244,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
         while (taken) {
           const int bit = __ffs(taken) - 1;
           taken &= taken - 1;
-          wl[cur][pos++] = (uint16_t)((w << 5) + bit);
+          *wl.at(cur, pos++) = (uint16_t)((w << 5) + bit);
         }
       }
       __syncthreads();
@@ -225,7 +254,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     items_total += n;
     // the current items leave the queue: improvements from now on re-queue them
     for (int i = tid; i < n; i += nthr) {
-      const int v = wl[cur][i];
+      const int v = *wl.at(cur, i);
       atomicAnd(&inq[v >> 5], ~(1u << (v & 31)));
     }
     if (tid == 0) sh.cnt[cur ^ 1] = 0;
@@ -236,7 +265,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
       bool app = false;
       int u = -1;
       if (idx < items) {
-        const int v = wl[cur][idx >> 3];
+        const int v = *wl.at(cur, idx >> 3);
         int k = idx & 7;
         k += (k >= 4);
         if (k_in_conn(g.conn, k)) {
@@ -259,7 +288,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
           }
         }
       }
-      warp_append(app, u, &sh.cnt[cur ^ 1], wl[cur ^ 1]);
+      warp_append(app, u, &sh.cnt[cur ^ 1], wl, cur ^ 1);
     }
     cur ^= 1;
     __syncthreads();
@@ -392,7 +421,18 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   }
   __syncthreads();
   // E4: descendant counts, deepest level first -- one warp, no block barriers
-  if (use_hist) {
+  // (shared-memory variant); block-wide per level in the global variant,
+  // where one warp would pay a global round trip per level and element
+  if (use_hist && !a.in_smem) {
+    for (int d = maxd; d >= 1; d--) {
+      const unsigned lo = vhist[d - 1], hi = vhist[d];
+      for (unsigned i = lo + tid; i < hi; i += nthr) {
+        const int v = order[i];
+        atomic_add_u16(szv, parent_of(v, vcode[v], g.W), (unsigned)vszv[v] + 1u);
+      }
+      __syncthreads();
+    }
+  } else if (use_hist) {
     if (wid == 0) {
       for (int d = maxd; d >= 1; d--) {
         const unsigned lo = vhist[d - 1], hi = vhist[d];
@@ -444,7 +484,12 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   // E6: preorder arrays.  tdp straight to global, then pre/szp staged in the
   // (now free) distance region for coalesced stores and the partition scan.
   float* gtdp = a.ts.tdp + off;
-  for (int v = tid; v < N; v += nthr) gtdp[pj[v] >> 16] = __uint_as_float(vdist[v]);
+  uint16_t* gtin = a.ts.tin + off;
+  for (int v = tid; v < N; v += nthr) {
+    const uint32_t q = pj[v] >> 16;
+    gtdp[q] = __uint_as_float(vdist[v]);
+    gtin[v] = (uint16_t)q;
+  }
   __syncthreads();
   volatile uint16_t* preS = reinterpret_cast<volatile uint16_t*>(base);
   volatile uint16_t* szS = preS + N;
@@ -464,8 +509,10 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   const int seg = (N + nthr - 1) / nthr;
   const int q0 = min(N, tid * seg), q1 = min(N, q0 + seg);
   unsigned lsum = 0, lpairs = 0;
+  // the root (q = 0) pairs with every pixel; the commit kernel fills its row
+  // with a grid-wide row scan, so its chunks are left out of the partition
   for (int q = q0; q < q1; q++) {
-    lsum += ((unsigned)szS[q] + 31u) >> 5;
+    lsum += q ? ((unsigned)szS[q] + 31u) >> 5 : 0u;
     lpairs += szS[q];
   }
   atomicAdd(&sh.pairs, lpairs);
@@ -499,7 +546,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   }
   unsigned run = (unsigned)sh.wsum[wid] + incl - lsum;
   for (int q = q0; q < q1; q++) {
-    const unsigned nch = ((unsigned)szS[q] + 31u) >> 5;
+    const unsigned nch = q ? ((unsigned)szS[q] + 31u) >> 5 : 0u;
     if (!nch) continue;
     // partitions p whose first chunk floor(p*T/P) lies in [run, run+nch)
     const unsigned long long plo = ((unsigned long long)run * P + T - 1) / T;
@@ -533,6 +580,11 @@ cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st) {
     if (e != cudaSuccess) return e;
   } else {
     a.scratch_bytes = prop_scratch_bytes(a.g.N);
+    const int NW = (a.g.N + 31) >> 5;
+    smem = 2 * align16((size_t)NW * 4) + 2 * (size_t)WL_SMEM * 2;
+    cudaError_t e = cudaFuncSetAttribute(k_propagate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
   }
   k_propagate<<<ntrees, 1024, smem, st>>>(a);
   return cudaGetLastError();
