@@ -574,7 +574,10 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
   } else {
     // ---- device commit loop with speculative propagation batches ----
     const int nblocks = commit_blocks(c);
-    const int nparts = nblocks * (commit_threads() / 32);
+    // work units per tree = UF x commit warps (dynamic balancing in k_commit)
+    int uf = N >= 32768 ? 4 : 1;
+    if (const char* e = getenv("GP_UNITS_PER_WARP")) uf = std::max(1, atoi(e));
+    const int nparts = nblocks * (commit_threads() / 32) * uf;
     int rts = ensure_tree_store(c, nparts);
     if (rts) return rts;
     int *d_slot_of = nullptr, *d_rank = nullptr, *d_ext = nullptr, *d_cands = nullptr;
@@ -659,7 +662,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     ca.ctl = d_ctl;
     ca.max_steps = N + 1;
     ca.bar = c->bar;
-    ca.staged = getenv("GP_STAGED") ? atoi(getenv("GP_STAGED")) : 0;
+
     ca.total_pairs = ((unsigned long long)N * N - N) / 2;
     PropArgs pa = base_prop(c);
     pa.src = d_cands;
@@ -675,10 +678,11 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     long long pdbg_n = 0;
     if (debug) {
       CUDA_TRY(dalloc(&d_pdbg, (size_t)K * 8));
-      CUDA_TRY(dalloc(&d_cdbg, (size_t)(N + 2) * 4));
-      CUDA_TRY(cudaMemsetAsync(d_cdbg, 0, (size_t)(N + 2) * 32, st));
+      CUDA_TRY(dalloc(&d_cdbg, (size_t)(N + 2) * 6));
+      CUDA_TRY(cudaMemsetAsync(d_cdbg, 0, (size_t)(N + 2) * 48, st));
       pa.dbg = d_pdbg;
       ca.dbg = d_cdbg;
+      ca.dbgw = d_cdbg + (size_t)(N + 2) * 4;
     }
     std::vector<EvPair> pev, cev;
     for (int guard = 0; guard < 4 * N + 8; guard++) {
@@ -742,12 +746,15 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
       std::vector<unsigned long long> h((size_t)(N + 2) * 4);
       CUDA_TRY(cudaMemcpy(h.data(), d_cdbg, h.size() * 8, cudaMemcpyDeviceToHost));
       if (const char* path = getenv("GP_DEBUG_DUMP")) {  // per-step stamps + new pairs
-        std::vector<unsigned long long> nw2(h_ctl.step);
+        std::vector<unsigned long long> nw2(h_ctl.step), hw((size_t)(N + 2) * 2);
         cudaMemcpy(nw2.data(), d_new, (size_t)h_ctl.step * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(hw.data(), ca.dbgw, hw.size() * 8, cudaMemcpyDeviceToHost);
+        const int nwarps = nblocks * (commit_threads() / 32);
         if (FILE* fp = fopen(path, "w")) {
           for (int i = 0; i < h_ctl.step; i++) {
             unsigned long long* r = &h[(size_t)i * 4];
-            fprintf(fp, "%d %llu %llu %llu %llu %llu\n", i, r[0], r[1], r[2], r[3], nw2[i]);
+            fprintf(fp, "%d %llu %llu %llu %llu %llu %llu %llu\n", i, r[0], r[1], r[2], r[3], nw2[i],
+                    hw[(size_t)i * 2], hw[(size_t)i * 2 + 1] / (unsigned long long)nwarps);
           }
           fclose(fp);
         }

@@ -99,7 +99,7 @@ __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned lo
   if (threadIdx.x == 0 && m != ~0ull) atomicMin(&a.selkey[step], m);
 }
 
-// K2 for one committed tree: this warp's share of the chunks.
+// K2 for one committed tree: one work unit (a contiguous range of chunks).
 //
 // The warp walks its chunk range window by window: one coalesced load brings
 // the metadata of 32 consecutive preorder positions (descendant count, pixel,
@@ -108,11 +108,10 @@ __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned lo
 // descendant-list loads and the G mark-word loads are each in flight
 // together (the fill is latency-bound: ~2 L2 round trips per G chunks).
 template <int G>
-__device__ __forceinline__ unsigned fill_warp_share(const CommitArgs& a, int slot, int s) {
+__device__ __forceinline__ unsigned fill_warp_share(const CommitArgs& a, int slot, int s, int p) {
   const int N = a.g.N;
   const int lane = threadIdx.x & 31;
   const int P = a.ts.nparts;
-  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const size_t off = (size_t)slot * N;
   const uint16_t* pre = a.ts.pre + off;
   const uint16_t* szp = a.ts.szp + off;
@@ -198,132 +197,6 @@ __device__ __forceinline__ unsigned fill_warp_share(const CommitArgs& a, int slo
         if (lane == 0 && nb && uu[j] != s) atomicAdd(&a.cnt[uu[j]], (int)nb);
         total_new += nb;
       }
-    }
-    count -= take;
-    q += 32;
-    coff = 0;
-  }
-  return lane == 0 ? total_new : 0u;
-}
-
-// K2 variant with asynchronous staging: the descendant ids of GS chunks are
-// loaded into registers together, then the GS x 32 mark words are gathered
-// with cp.async straight into this warp's shared-memory stage (no register
-// per in-flight load), so a warp needs ~2 memory round trips per GS chunks.
-// cp.async.ca caches in L1; every grid barrier's gpu-scope fence invalidates
-// L1, and a pair's own bit only changes by its own (single) test in a step.
-__device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gsrc) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-template <int GS>
-__device__ __forceinline__ unsigned fill_warp_staged(const CommitArgs& a, int slot, int s,
-                                                     uint32_t* stage /* [GS][32] */) {
-  const int N = a.g.N;
-  const int lane = threadIdx.x & 31;
-  const int P = a.ts.nparts;
-  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const size_t off = (size_t)slot * N;
-  const uint16_t* pre = a.ts.pre + off;
-  const uint16_t* szp = a.ts.szp + off;
-  const float* tdp = a.ts.tdp + off;
-  const unsigned T = __ldg(&a.ts.T[slot]);
-  const unsigned b0 = (unsigned)(((unsigned long long)p * T) / P);
-  const unsigned b1 = (unsigned)(((unsigned long long)(p + 1) * T) / P);
-  unsigned count = b1 - b0;
-  if (!count) return 0;
-  const uint32_t pw = __ldg(&a.ts.part[(size_t)slot * P + p]);
-  int q = (int)(pw & 0xFFFFu);
-  unsigned coff = pw >> 16;
-  unsigned total_new = 0;
-  const MarkLayout L = a.L;
-  while (count) {
-    const int qa = q + lane;
-    unsigned sz_l = 0;
-    int u_l = 0;
-    float td_l = 0.f;
-    if (qa < N) {
-      sz_l = __ldg(&szp[qa]);
-      u_l = __ldg(&pre[qa]);
-      td_l = __ldg(&tdp[qa]);
-    }
-    unsigned nch_l = qa ? (sz_l + 31u) >> 5 : 0u;
-    unsigned c0_l = 0;
-    if (lane == 0) { nch_l -= coff; c0_l = coff; }
-    const bool full_l = nch_l && u_l != s && __ldcg(&a.cnt[u_l]) >= N - 1;
-    unsigned cum = nch_l;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xffffffffu, cum, o);
-      if (lane >= o) cum += y;
-    }
-    const unsigned excl = cum - nch_l;
-    const unsigned wtotal = __shfl_sync(0xffffffffu, cum, 31);
-    const unsigned take = min(wtotal, count);
-    for (unsigned cb = 0; cb < take; cb += GS) {
-      uint32_t w[GS];
-      unsigned okm = 0;
-      // A: descendant ids of GS chunks, all loads in flight together
-#pragma unroll
-      for (int j = 0; j < GS; j++) {
-        const unsigned c = cb + j;
-        const unsigned bm = __ballot_sync(0xffffffffu, cum > c);
-        const int ol = bm ? __ffs(bm) - 1 : 0;
-        const unsigned sz = __shfl_sync(0xffffffffu, sz_l, ol);
-        const unsigned cidx = __shfl_sync(0xffffffffu, c0_l + (c - excl), ol);
-        const bool full = __shfl_sync(0xffffffffu, (int)full_l, ol);
-        const unsigned k = cidx * 32u + lane;
-        const bool ok = c < take && !full && k < sz;
-        w[j] = ok ? (uint32_t)__ldg(&pre[q + ol + 1 + k]) : 0u;
-        okm |= (unsigned)ok << j;
-      }
-      // B: mark words -> shared stage (asynchronous gathers)
-#pragma unroll
-      for (int j = 0; j < GS; j++) {
-        const unsigned bm = __ballot_sync(0xffffffffu, cum > cb + j);
-        const int ol = bm ? __ffs(bm) - 1 : 0;
-        const int u = __shfl_sync(0xffffffffu, u_l, ol);
-        if ((okm >> j) & 1u) {
-          const uint32_t wcol = mcol(L, w[j]);
-          cp_async4(&stage[j * 32 + lane], a.mark + (size_t)u * L.RW + (wcol >> 5));
-        }
-      }
-      cp_async_wait_all();
-      __syncwarp();
-      // C: test and fill
-#pragma unroll
-      for (int j = 0; j < GS; j++) {
-        const unsigned c = cb + j;
-        const unsigned bm = __ballot_sync(0xffffffffu, cum > c);
-        const int ol = bm ? __ffs(bm) - 1 : 0;
-        const int u = __shfl_sync(0xffffffffu, u_l, ol);
-        const float tdu = __shfl_sync(0xffffffffu, td_l, ol);
-        const unsigned cidx = __shfl_sync(0xffffffffu, c0_l + (c - excl), ol);
-        bool isnew = false;
-        if ((okm >> j) & 1u) {
-          const uint32_t wcol = mcol(L, w[j]);
-          const uint32_t wbit = 1u << (wcol & 31);
-          isnew = !(stage[j * 32 + lane] & wbit);
-          if (isnew) {
-            const int ww = (int)w[j];
-            const uint32_t ucol = mcol(L, (uint32_t)u);
-            atomicOr(a.mark + (size_t)u * L.RW + (wcol >> 5), wbit);
-            atomicOr(a.mark + mword(L, (uint32_t)ww, ucol), 1u << (ucol & 31));
-            const float duv = __fsub_rn(__ldg(&tdp[q + ol + 1 + cidx * 32u + lane]), tdu);
-            a.D[(size_t)u * N + ww] = duv;
-            a.D[(size_t)ww * N + u] = duv;
-            atomicAdd(&a.cnt[ww], 1);
-          }
-        }
-        const unsigned nb = __popc(__ballot_sync(0xffffffffu, isnew));
-        if (lane == 0 && nb && u != s) atomicAdd(&a.cnt[u], (int)nb);
-        total_new += nb;
-      }
-      __syncwarp();
     }
     count -= take;
     q += 32;
@@ -465,9 +338,9 @@ __device__ __forceinline__ void compact_list(const CommitArgs& a, unsigned cur, 
 template <int G, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   __shared__ unsigned long long red64[32];
-  constexpr int GS = 16;
-  __shared__ uint32_t stage_all[THREADS / 32][GS * 32];
-  uint32_t* stage = stage_all[threadIdx.x >> 5];
+  __shared__ int unit_ctr[2];  // per-CTA work-unit counters (alternating steps)
+  if (threadIdx.x == 0) unit_ctr[0] = unit_ctr[1] = 0;
+  __syncthreads();
   const int N = a.g.N;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const bool keeper = gtid == 0;  // bookkeeping thread (registers, stores only)
@@ -507,14 +380,43 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     if (slot < 0) { status = CTL_MISS; break; }
     unsigned long long* dbg = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + (size_t)step * 4 : nullptr;
     if (dbg) dbg[0] = gtimer();
+    const unsigned long long tw0 = a.dbgw ? gtimer() : 0ull;
     const unsigned cslot = keeper ? __ldg(&a.ts.C[slot]) : 0u;  // consumed at step end
     // ---- K2: fill ----
-    unsigned long long lnew =
-        mode == 1 ? (unsigned long long)fill_list(a, slot, s, lcur, ln)
-        : a.staged ? (unsigned long long)fill_warp_staged<GS>(a, slot, s, stage)
-                   : (unsigned long long)fill_warp_share<G>(a, slot, s);
+    unsigned long long lnew = 0;
+    if (mode == 1) {
+      lnew = fill_list(a, slot, s, lcur, ln);
+    } else {
+      // Work units of this tree are interleaved over the CTAs (unit = b + k *
+      // nblocks) and pulled by the CTA's warps from a shared counter, so the
+      // expensive units (rows with many new pairs) do not pile on one warp.
+      const int lane = threadIdx.x & 31;
+      const int PU = a.ts.nparts;
+      const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
+      if (PU <= nwarps) {  // one unit per warp: static
+        const int u = (int)blockIdx.x * (int)(blockDim.x >> 5) + (int)(threadIdx.x >> 5);
+        if (u < PU) lnew = fill_warp_share<G>(a, slot, s, u);
+      } else {
+        int* ctr = &unit_ctr[step & 1];
+        int k = lane == 0 ? atomicAdd(ctr, 1) : 0;
+        k = __shfl_sync(0xffffffffu, k, 0);
+        for (;;) {
+          const int u = (int)blockIdx.x + k * (int)gridDim.x;
+          if (u >= PU) break;
+          int nk = lane == 0 ? atomicAdd(ctr, 1) : 0;
+          lnew += fill_warp_share<G>(a, slot, s, u);
+          k = __shfl_sync(0xffffffffu, nk, 0);
+        }
+        if (threadIdx.x == 0) unit_ctr[(step & 1) ^ 1] = 0;  // next step's counter
+      }
+    }
     if (mode == 0) lnew += fill_root_row(a, slot, s);
     if (dbg) dbg[1] = gtimer();
+    if (a.dbgw && (threadIdx.x & 31) == 0) {
+      const unsigned long long dt = gtimer() - tw0;
+      atomicMax(&a.dbgw[(size_t)step * 2], dt);
+      atomicAdd(&a.dbgw[(size_t)step * 2 + 1], dt);
+    }
     lnew = block_reduce_sum(lnew, red64);
     if (threadIdx.x == 0 && lnew) atomicAdd(&a.newp[step], lnew);
     grid_barrier(a.bar, gen);

@@ -100,10 +100,10 @@ struct CommitArgs {
   Ctl* ctl;
   int max_steps;           // commits allowed in this launch
   unsigned long long* dbg; // optional per-step stamps [steps][4] from block 0 (debug)
+  unsigned long long* dbgw; // optional per-step warp fill times [steps][2] = (max, sum) ns
   GridBarrier* bar;
   uint32_t* plist[2];      // unfilled pairs (u << 16 | w, u < w), list mode
   unsigned long long total_pairs;
-  int staged;              // range fill via cp.async staging (1) or registers (0)
 };
 
 int commit_threads();

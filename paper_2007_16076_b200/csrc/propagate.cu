@@ -42,6 +42,7 @@ extern __shared__ __align__(16) unsigned char g_smem[];
 
 constexpr int HIST_SMEM = 4096;  // depth-histogram bins in the shared-memory variant
 constexpr int WL_SMEM = 12288;   // worklist entries kept in smem (global-scratch variant)
+constexpr int BIG_MAX = 64;      // queued many-unit preorder positions (partition writes)
 
 struct PropShared {
   int cnt[2];
@@ -51,6 +52,8 @@ struct PropShared {
   int wsum[32];
   unsigned total;
   unsigned pairs;
+  int nbig;
+  unsigned big[64][4];
 };
 
 struct Layout {
@@ -545,17 +548,47 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     a.ts.C[slot] = sh.pairs;
   }
   unsigned run = (unsigned)sh.wsum[wid] + incl - lsum;
+  // smallest p with p*T >= x*P (= ceil(x*P/T)): double estimate, exact fix-up
+  auto first_part = [&](unsigned long long x) -> unsigned long long {
+    if (!T) return P;
+    unsigned long long pp = (unsigned long long)((double)x * (double)P / (double)T);
+    while (pp > 0 && (pp - 1) * T >= x * P) pp--;
+    while (pp * T < x * P) pp++;
+    return pp;
+  };
+  auto write_part = [&](unsigned long long pp, unsigned q, unsigned runq) {
+    const unsigned long long num = pp * T;
+    unsigned b = (unsigned)((double)num / (double)P);  // floor(p*T/P), exact fix-up
+    while ((unsigned long long)b * P > num) b--;
+    while ((unsigned long long)(b + 1) * P <= num) b++;
+    gpart[pp] = (uint32_t)q | ((b - runq) << 16);
+  };
+  // positions owning many units (near the root) are queued and written by
+  // whole warps; the rest by their thread
+  if (tid == 0) sh.nbig = 0;
+  __syncthreads();
   for (int q = q0; q < q1; q++) {
     const unsigned nch = q ? ((unsigned)szS[q] + 31u) >> 5 : 0u;
     if (!nch) continue;
     // partitions p whose first chunk floor(p*T/P) lies in [run, run+nch)
-    const unsigned long long plo = ((unsigned long long)run * P + T - 1) / T;
-    const unsigned long long phi = (((unsigned long long)(run + nch) * P + T - 1) / T);
-    for (unsigned long long pp = plo; pp < phi && pp < P; pp++) {
-      const unsigned b = (unsigned)((pp * T) / P);
-      gpart[pp] = (uint32_t)q | ((b - run) << 16);
+    const unsigned long long plo = first_part(run), phi = min(first_part(run + nch), P);
+    if (phi - plo > 32) {
+      const int i = atomicAdd(&sh.nbig, 1);
+      if (i < BIG_MAX) {
+        sh.big[i][0] = (unsigned)q; sh.big[i][1] = run;
+        sh.big[i][2] = (unsigned)plo; sh.big[i][3] = (unsigned)phi;
+        run += nch;
+        continue;
+      }
     }
+    for (unsigned long long pp = plo; pp < phi; pp++) write_part(pp, (unsigned)q, run);
     run += nch;
+  }
+  __syncthreads();
+  const int nbig = min(sh.nbig, BIG_MAX);
+  for (int i = wid; i < nbig; i += nthr >> 5) {
+    for (unsigned pp = sh.big[i][2] + lane; pp < sh.big[i][3]; pp += 32)
+      write_part(pp, sh.big[i][0], sh.big[i][1]);
   }
   if (dbg) {
     __syncthreads();
