@@ -47,6 +47,8 @@ struct gp_ctx {
   int commit_blocks = 0;
   double mean_w = 1.0;  // mean edge weight (bucket width scale)
   uint32_t* list[2] = {nullptr, nullptr};  // unfilled-pair lists (late phase)
+  void* ws[32] = {};      // run workspace, cached across runs (no cudaMalloc in gp_run)
+  size_t ws_bytes[32] = {};
   size_t list_cap = 0;
   GridBarrier* bar = nullptr;
 };
@@ -164,6 +166,7 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
   cudaFree(c->ts.tin);
   cudaFree(c->list[0]);
   cudaFree(c->list[1]);
+  for (void* p : c->ws) cudaFree(p);
   cudaFree(c->bar);
   cudaFree(c->scratch);
   if (c->st) cudaStreamDestroy(c->st);
@@ -171,6 +174,24 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
 }
 
 extern "C" int gp_ctx_num_pixels(const gp_ctx* c) { return c ? c->g.N : 0; }
+
+enum { WS_SEQ, WS_NEW, WS_SRC, WS_SLOT_OF, WS_RANK, WS_EXT, WS_SELKEY, WS_FLAGS, WS_CTL, WS_DFC,
+       WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB };
+
+template <typename T>
+static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
+  const size_t bytes = count * sizeof(T) + 16;
+  if (c->ws_bytes[id] < bytes) {
+    cudaFree(c->ws[id]);
+    c->ws[id] = nullptr;
+    c->ws_bytes[id] = 0;
+    cudaError_t e = cudaMalloc(&c->ws[id], bytes);
+    if (e != cudaSuccess) return e;
+    c->ws_bytes[id] = bytes;
+  }
+  *p = reinterpret_cast<T*>(c->ws[id]);
+  return cudaSuccess;
+}
 
 static int ensure_scratch(gp_ctx* c, size_t ntrees) {
   if (prop_fits_smem(c->g.N) || ntrees <= c->scratch_trees) return GP_OK;
@@ -281,9 +302,9 @@ static int extrema_device(gp_ctx* c, int* centroid, float* dfc_dev, std::vector<
   float* d_fb = nullptr;
   int rc = ensure_scratch(c, 1);
   if (rc) return rc;
-  CUDA_TRY(dalloc(&d_src, border.size() + 1));
-  CUDA_TRY(dalloc(&d_cen, 1));
-  CUDA_TRY(dalloc(&d_fb, N));
+  CUDA_TRY(ws_get(c, WS_BORDER, &d_src, border.size() + 1));
+  CUDA_TRY(ws_get(c, WS_CEN, &d_cen, 1));
+  CUDA_TRY(ws_get(c, WS_FB, &d_fb, N));
   CUDA_TRY(cudaMemcpyAsync(d_src, border.data(), border.size() * 4, cudaMemcpyHostToDevice, c->st));
   PropArgs a = base_prop(c);
   a.src = d_src;
@@ -302,9 +323,6 @@ static int extrema_device(gp_ctx* c, int* centroid, float* dfc_dev, std::vector<
   CUDA_TRY(cudaMemcpyAsync(centroid, d_cen, 4, cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(cudaMemcpyAsync(dfc_host.data(), dfc_dev, N * 4, cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(cudaStreamSynchronize(c->st));
-  cudaFree(d_src);
-  cudaFree(d_cen);
-  cudaFree(d_fb);
   return GP_OK;
 }
 
@@ -535,8 +553,8 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
 
   int* d_seq = nullptr;
   unsigned long long* d_new = nullptr;
-  CUDA_TRY(dalloc(&d_seq, N));
-  CUDA_TRY(dalloc(&d_new, N));
+  CUDA_TRY(ws_get(c, WS_SEQ, &d_seq, N));
+  CUDA_TRY(ws_get(c, WS_NEW, &d_new, N));
   CUDA_TRY(cudaMemsetAsync(d_new, 0, (size_t)N * 8, st));
   int P = 0;
   int rc = GP_OK;
@@ -549,7 +567,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     std::vector<int32_t> srcs(N - 1);
     for (int i = 0; i < N - 1; i++) srcs[i] = i;
     int* d_src = nullptr;
-    CUDA_TRY(dalloc(&d_src, N));
+    CUDA_TRY(ws_get(c, WS_SRC, &d_src, N));
     CUDA_TRY(cudaMemcpyAsync(d_src, srcs.data(), (N - 1) * 4, cudaMemcpyHostToDevice, st));
     EvPair pp;
     cudaEventCreate(&pp.a); cudaEventCreate(&pp.b);
@@ -569,7 +587,6 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     S.batches = 1;
     S.kernels += 2;
     P = N - 1;
-    cudaFree(d_src);
     cudaEventDestroy(pp.a); cudaEventDestroy(pp.b);
   } else {
     // ---- device commit loop with speculative propagation batches ----
@@ -585,16 +602,16 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     unsigned long long* d_selkey = nullptr;
     Ctl* d_ctl = nullptr;
     float* d_dfc = nullptr;
-    CUDA_TRY(dalloc(&d_slot_of, N));
-    CUDA_TRY(dalloc(&d_rank, N));
-    CUDA_TRY(dalloc(&d_ext, N));
-    CUDA_TRY(dalloc(&d_selkey, N + 2));
+    CUDA_TRY(ws_get(c, WS_SLOT_OF, &d_slot_of, N));
+    CUDA_TRY(ws_get(c, WS_RANK, &d_rank, N));
+    CUDA_TRY(ws_get(c, WS_EXT, &d_ext, N));
+    CUDA_TRY(ws_get(c, WS_SELKEY, &d_selkey, N + 2));
     unsigned* d_flags = nullptr;
-    CUDA_TRY(dalloc(&d_flags, N + 2));
+    CUDA_TRY(ws_get(c, WS_FLAGS, &d_flags, N + 2));
     CUDA_TRY(cudaMemsetAsync(d_flags, 0, (size_t)(N + 2) * 4, st));
-    CUDA_TRY(dalloc(&d_ctl, 1));
-    CUDA_TRY(dalloc(&d_dfc, N));
-    CUDA_TRY(dalloc(&d_free, N));
+    CUDA_TRY(ws_get(c, WS_CTL, &d_ctl, 1));
+    CUDA_TRY(ws_get(c, WS_DFC, &d_dfc, N));
+    CUDA_TRY(ws_get(c, WS_FREE, &d_free, N));
     if (!c->bar) CUDA_TRY(dalloc(&c->bar, 1));
     CUDA_TRY(cudaMemsetAsync(c->bar, 0, sizeof(GridBarrier), st));
     {
@@ -638,8 +655,8 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     if (spec_k <= 0)
       if (const char* e = getenv("GP_SPEC_K")) K = atoi(e);
     K = std::min(K, N);
-    CUDA_TRY(dalloc(&d_cands, K));
-    CUDA_TRY(dalloc(&d_slots, K));
+    CUDA_TRY(ws_get(c, WS_CANDS, &d_cands, K));
+    CUDA_TRY(ws_get(c, WS_SLOTS, &d_slots, K));
     int rcs = ensure_scratch(c, (size_t)K);
     if (rcs) return rcs;
     CommitArgs ca;
@@ -786,8 +803,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     for (auto& e : cev) { S.ms_commit += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (auto& e : pev) { S.ms_propagate += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     P = h_ctl.step;
-    cudaFree(d_slot_of); cudaFree(d_rank); cudaFree(d_ext); cudaFree(d_cands); cudaFree(d_slots);
-    cudaFree(d_selkey); cudaFree(d_ctl); cudaFree(d_dfc); cudaFree(d_free); cudaFree(d_flags);
+
     S.propagations += h_ctl.total_props;
     S.visits = (int64_t)h_ctl.visits;
   }
@@ -795,7 +811,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
   S.ms_setup = ev_ms(setup);
   cudaEventDestroy(tot.a); cudaEventDestroy(tot.b);
   cudaEventDestroy(setup.a); cudaEventDestroy(setup.b);
-  if (rc) { cudaFree(d_seq); cudaFree(d_new); return rc; }
+  if (rc) return rc;
   std::vector<unsigned long long> nw(P > 0 ? P : 1);
   if (P > 0) CUDA_TRY(cudaMemcpy(nw.data(), d_new, (size_t)P * 8, cudaMemcpyDeviceToHost));
   if (seq_out && P > 0) CUDA_TRY(cudaMemcpy(seq_out, d_seq, (size_t)P * 4, cudaMemcpyDeviceToHost));
@@ -804,8 +820,6 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     filled += (int64_t)nw[i];
     if (new_out) new_out[i] = (int64_t)nw[i];
   }
-  cudaFree(d_seq);
-  cudaFree(d_new);
   s->filled = filled;
   S.raw_count = P;
   S.adjusted_count = P + (strategy == GP_STRATEGY_FILLING_RATE ? 2 : 0);

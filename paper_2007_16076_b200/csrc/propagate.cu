@@ -33,6 +33,9 @@
 // of the fill work into commit warps (exclusive scan of 32-pair chunks; the
 // root's N-1 pairs are excluded -- the commit kernel scans its row).  All
 // of it runs here, off the commit loop's critical path.
+#include <algorithm>
+#include <cstdlib>
+
 #include "gp_common.cuh"
 #include "gp_kernels.h"
 
@@ -619,7 +622,13 @@ cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st) {
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k_propagate<<<ntrees, 1024, smem, st>>>(a);
+  // One tree per CTA.  Trees are latency-bound, so two 512-thread CTAs per SM
+  // beat one 1024-thread CTA whenever shared memory admits two (registers:
+  // 2 x 512 x <=64); 128x128 maps need ~212 KB and keep 1024 threads.
+  const size_t per_cta = smem + 1024 + sizeof(PropShared);
+  int threads = (228 * 1024) / per_cta >= 2 ? 512 : 1024;
+  if (const char* e = getenv("GP_PROP_THREADS")) threads = std::max(128, std::min(1024, atoi(e)));
+  k_propagate<<<ntrees, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
