@@ -161,6 +161,20 @@ def run_reference(args, spec, img, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def aggregate(total_ms: float, pairs_per_image: int, steps: int, world: int, dist=None,
+              device=None) -> tuple[float, float]:
+    """Whole-job throughput over `world` replica ranks: (max-over-ranks total
+    device ms, value = world * A * K / that time).  `dist` is
+    torch.distributed (nccl on the GPU box, gloo in the CPU tests)."""
+    if dist is not None and world > 1:
+        import torch
+
+        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    return total_ms, world * pairs_per_image * steps / (total_ms / 1e3)
+
+
 def _other_configs(L, _lib, skip: int):
     """One device-timed run of every other BASELINE config (not the headline)."""
     out = {}
@@ -259,13 +273,8 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    total_ms = sum(r.ms_total for r in runs)
-    if dist:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms, value = aggregate(sum(r.ms_total for r in runs), A, args.steps, world, dist, "cuda")
     ms_step = total_ms / args.steps
-    value = world * A * args.steps / (total_ms / 1e3)
     r0 = runs[-1]
     P = int(r0.raw_count)
     C = int(r0.visits)

@@ -1,0 +1,56 @@
+"""CPU: the multi-rank (replicas) aggregation of bench.py over gloo, world_size 2.
+
+The path does not shard (replicas only); what runs across ranks
+is the max-over-ranks timing and the whole-job throughput formula.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+
+    local_ms = 100.0 * (rank + 1)  # rank 1 is the slow one
+    total_ms, value = bench.aggregate(local_ms, pairs_per_image=1000, steps=4, world=world,
+                                      dist=dist, device="cpu")
+    q.put((rank, total_ms, value))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_replica_aggregation_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(2))
+    for _, total_ms, value in res:
+        assert total_ms == pytest.approx(200.0)  # max over ranks
+        assert value == pytest.approx(2 * 1000 * 4 / 0.2)
+
+
+def test_aggregation_single_rank():
+    import bench
+
+    total_ms, value = bench.aggregate(500.0, 10, 5, 1)
+    assert total_ms == 500.0 and value == pytest.approx(100.0)

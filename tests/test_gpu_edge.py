@@ -1,0 +1,108 @@
+"""GPU: edge cases and invariances of the device path (against the oracle)."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _seq(run):
+    return [s for _, s, _ in run.trace.samples]
+
+
+@pytest.mark.parametrize("shape", [(1, 2), (1, 7), (9, 1), (2, 2), (3, 1), (2, 5), (17, 3)])
+def test_degenerate_shapes(gp, oracle, shape):
+    img = np.random.default_rng(sum(shape)).integers(1, 256, shape)
+    for kind, k in (("filling-rate", gp.StrategyKind.FILLING_RATE), ("naive", gp.StrategyKind.NAIVE)):
+        o = oracle.run(img, kind)
+        run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, k)
+        assert _seq(run) == o["seq"].tolist()
+        assert np.array_equal(run.distances.dist, o["D"])
+        assert run.trace.adjusted_count == o["adjusted"]
+
+
+def test_mean_metric_runs(gp, oracle):
+    img = np.random.default_rng(3).integers(1, 256, (11, 13))
+    o = oracle.run(img, "filling-rate", metric="mean")
+    run = gp.run_strategy(gp.Image(img), gp.Metric.MEAN, gp.StrategyKind.FILLING_RATE)
+    assert _seq(run) == o["seq"].tolist()
+    assert np.array_equal(run.distances.dist, o["D"])
+
+
+def test_naive_with_tree(gp, oracle):
+    img = np.random.default_rng(5).integers(1, 256, (9, 10))
+    o = oracle.run(img, "naive", naive_with_tree=True)
+    run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, gp.StrategyKind.NAIVE, naive_with_tree=True)
+    assert _seq(run) == o["seq"].tolist()
+    assert np.array_equal(run.distances.dist, o["D"])
+    plain = gp.run_strategy(gp.Image(img), gp.Metric.SUM, gp.StrategyKind.NAIVE)
+    assert run.trace.raw_count <= plain.trace.raw_count  # test_strategies.py:335-342
+
+
+def test_fp32_single_zero_pixel_and_ties(gp, oracle):
+    rng = np.random.default_rng(9)
+    img = (rng.integers(1, 4, (14, 12)) / 4).astype(np.float32)
+    img[5, 5] = 0.0
+    for conn in (8, 4):
+        o = oracle.run(img, "filling-rate", conn=conn)
+        run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, gp.StrategyKind.FILLING_RATE,
+                              connectivity=conn)
+        assert _seq(run) == o["seq"].tolist()
+        assert np.array_equal(run.distances.dist, o["D"])
+
+
+def test_l1_distances_exact(gp, oracle):
+    rng = np.random.default_rng(10)
+    img = rng.integers(1, 4, (8, 9))  # many zero-weight edges
+    graph = gp.GridGraph(gp.Image(img), gp.Metric.L1)
+    for s in range(0, img.size, 7):
+        d, _ = oracle.propagate(img, [s], metric="l1")
+        r = graph.propagate([s])
+        assert np.array_equal(r.dist, d)
+        # parents form a valid shortest-path forest even where heap order is not pinned
+        for v in range(img.size):
+            p = int(r.parent[v])
+            if p >= 0:
+                assert r.dist[v] == r.dist[p] + gp.edge_weight(gp.Image(img), gp.Metric.L1, p, v)
+
+
+@pytest.mark.parametrize("env", [
+    {"GP_SPEC_K": "7"}, {"GP_SPEC_K": "1000"}, {"GP_LIST_ALPHA": "0"}, {"GP_LIST_ALPHA": "1000"},
+    {"GP_UNITS_PER_WARP": "4"}, {"GP_DELTA_FACTOR": "inf"}, {"GP_DELTA_FACTOR": "0.5"},
+    {"GP_PROP_THREADS": "256"}, {"GP_BARRIER": "sw"},
+])
+def test_tuning_knobs_do_not_change_results(gp, oracle, env, monkeypatch):
+    img = np.random.default_rng(11).random((24, 20), dtype=np.float32)
+    o = oracle.run(img, "filling-rate")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, gp.StrategyKind.FILLING_RATE)
+    assert _seq(run) == o["seq"].tolist()
+    assert np.array_equal(run.distances.dist, o["D"])
+    assert np.array_equal(run.distances.point_filled_counts, np.full(img.size, img.size - 1))
+
+
+def test_brute_force_oracle_and_apgd(gp):
+    img = gp.Image(np.random.default_rng(12).integers(1, 256, (7, 7)))
+    bf = gp.brute_force_oracle(img)
+    fr = gp.run_strategy(img, gp.Metric.SUM, gp.StrategyKind.FILLING_RATE)
+    assert np.array_equal(bf.dist, fr.distances.dist)
+    blob = fr.distances.to_bytes()
+    assert blob[:4] == gp.APGD_MAGIC and blob[4] == 1
+    n = img.size
+    grid = np.frombuffer(blob, dtype="<u8", offset=9).reshape(n, n)
+    assert np.array_equal(grid.astype(np.int64), bf.dist)
+
+
+def test_metric_properties_of_completed_array(gp):
+    # test_acceptance.py:519-531: symmetric, zero diagonal, triangle inequality
+    img = gp.Image(np.random.default_rng(13).integers(1, 256, (15, 15)))
+    D = gp.run_strategy(img, gp.Metric.SUM, gp.StrategyKind.FILLING_RATE).distances.dist
+    assert np.array_equal(D, D.T) and (np.diag(D) == 0).all()
+    rng = np.random.default_rng(9)
+    x, y, z = (rng.integers(0, D.shape[0], 10_000) for _ in range(3))
+    assert int((D[x, z] > D[x, y] + D[y, z]).sum()) == 0
