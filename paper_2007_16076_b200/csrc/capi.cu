@@ -681,12 +681,14 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     ca.bar = c->bar;
 
     ca.total_pairs = ((unsigned long long)N * N - N) / 2;
+
     PropArgs pa = base_prop(c);
     pa.src = d_cands;
     pa.ns = 1;
     pa.ntrees_dev = &d_ctl->ncand;
     pa.slot = d_slots;
     pa.ts = c->ts;
+    pa.L = L;
     pa.delta = default_delta(c);
     // debug phase stamps (GP_DEBUG=1): per tree of the batches, per step
     const bool debug = getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"));

@@ -99,21 +99,21 @@ __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned lo
   if (threadIdx.x == 0 && m != ~0ull) atomicMin(&a.selkey[step], m);
 }
 
-// K2 for one committed tree: one work unit (a contiguous range of chunks).
-//
-// The warp walks its chunk range window by window: one coalesced load brings
-// the metadata of 32 consecutive preorder positions (descendant count, pixel,
-// distance, full-row flag), a warp scan of the chunk counts maps chunks to
-// positions, and the chunks are then processed G at a time so that the G
-// descendant-list loads and the G mark-word loads are each in flight
-// together (the fill is latency-bound: ~2 L2 round trips per G chunks).
-template <int G>
-__device__ __forceinline__ unsigned fill_warp_share(const CommitArgs& a, int slot, int s, int p) {
+// K2 for one committed tree: one work unit = chunks [b0, b1) of the tree's
+// chunk sequence (32 consecutive descendants of one preorder position).
+// The warp scans 32 preorder positions at a time (descendant counts, packed
+// (tile column << 16 | pixel) entries, full-row flags), then walks the
+// positions that own chunks; for each ancestor u (uniform across the warp)
+// the inner loop is load entry -> load mark word of row u -> test bit, U
+// iterations in flight.  The fill is instruction-issue bound, so the loop is
+// kept to a handful of instructions per tested pair.
+template <int U>
+__device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int s, int p) {
   const int N = a.g.N;
   const int lane = threadIdx.x & 31;
   const int P = a.ts.nparts;
   const size_t off = (size_t)slot * N;
-  const uint16_t* pre = a.ts.pre + off;
+  const uint32_t* pre = a.ts.pre + off;
   const uint16_t* szp = a.ts.szp + off;
   const float* tdp = a.ts.tdp + off;
   const unsigned T = __ldg(&a.ts.T[slot]);
@@ -127,76 +127,72 @@ __device__ __forceinline__ unsigned fill_warp_share(const CommitArgs& a, int slo
   unsigned total_new = 0;
   const MarkLayout L = a.L;
   while (count) {
-    // ---- window metadata, one position per lane ----
     const int qa = q + lane;
     unsigned sz_l = 0;
-    int u_l = 0;
-    float td_l = 0.f;
+    uint32_t e_l = 0;
     if (qa < N) {
       sz_l = __ldg(&szp[qa]);
-      u_l = __ldg(&pre[qa]);
-      td_l = __ldg(&tdp[qa]);
+      e_l = __ldg(&pre[qa]);
     }
     unsigned nch_l = qa ? (sz_l + 31u) >> 5 : 0u;  // root row: see fill_root_row
     unsigned c0_l = 0;
     if (lane == 0) { nch_l -= coff; c0_l = coff; }
-    const bool full_l = nch_l && u_l != s && __ldcg(&a.cnt[u_l]) >= N - 1;
     unsigned cum = nch_l;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned y = __shfl_up_sync(0xffffffffu, cum, o);
       if (lane >= o) cum += y;
     }
+    const unsigned take = min(__shfl_sync(0xffffffffu, cum, 31), count);
     const unsigned excl = cum - nch_l;
-    const unsigned wtotal = __shfl_sync(0xffffffffu, cum, 31);
-    const unsigned take = min(wtotal, count);
-    // ---- chunks, G at a time ----
-    for (unsigned cb = 0; cb < take; cb += G) {
-      int w[G], qc[G], uu[G];
-      bool ok[G];
-      float tdu[G];
+    const unsigned mych = excl < take ? min(nch_l, take - excl) : 0u;
+    const int u_l = (int)(e_l & 0xFFFFu);
+    const bool full_l = mych && u_l != s && __ldcg(&a.cnt[u_l]) >= N - 1;
+    unsigned work = __ballot_sync(0xffffffffu, mych && !full_l);
+    while (work) {
+      const int ol = __ffs(work) - 1;
+      work &= work - 1;
+      const uint32_t eu = __shfl_sync(0xffffffffu, e_l, ol);
+      const unsigned sz = __shfl_sync(0xffffffffu, sz_l, ol);
+      const unsigned c0 = __shfl_sync(0xffffffffu, c0_l, ol);
+      const unsigned nc = __shfl_sync(0xffffffffu, mych, ol);
+      const int u = (int)(eu & 0xFFFFu);
+      const uint32_t ucol = eu >> 16;
+      uint32_t* mrow = a.mark + (size_t)u * L.RW;
+      const int qb = q + ol + 1;  // preorder position of the first descendant
+      const unsigned kend = min(sz, (c0 + nc) * 32u);
+      unsigned unew = 0;
+      for (unsigned kb = c0 * 32u; kb < kend; kb += 32u * U) {  // warp-uniform trips
+        uint32_t ew[U], word[U];
 #pragma unroll
-      for (int j = 0; j < G; j++) {
-        const unsigned c = cb + j;
-        const unsigned m = __ballot_sync(0xffffffffu, cum > c);
-        const int ol = m ? __ffs(m) - 1 : 0;
-        const unsigned sz = __shfl_sync(0xffffffffu, sz_l, ol);
-        const unsigned cidx = __shfl_sync(0xffffffffu, c0_l + (c - excl), ol);
-        const bool full = __shfl_sync(0xffffffffu, (int)full_l, ol);
-        uu[j] = __shfl_sync(0xffffffffu, u_l, ol);
-        tdu[j] = __shfl_sync(0xffffffffu, td_l, ol);
-        qc[j] = q + ol;
-        const unsigned k = cidx * 32u + lane;
-        ok[j] = c < take && !full && k < sz;
-        w[j] = ok[j] ? (int)__ldg(&pre[qc[j] + 1 + k]) : 0;
-        qc[j] += 1 + (int)k;  // preorder position of w
-      }
-      uint32_t word[G], wbit[G];
-      uint32_t* mw[G];
-#pragma unroll
-      for (int j = 0; j < G; j++) {
-        const uint32_t wcol = mcol(L, (uint32_t)w[j]);
-        wbit[j] = 1u << (wcol & 31);
-        mw[j] = a.mark + (size_t)uu[j] * L.RW + (wcol >> 5);
-        word[j] = ok[j] ? __ldcg(mw[j]) : wbit[j];
-      }
-#pragma unroll
-      for (int j = 0; j < G; j++) {
-        const bool isnew = !(word[j] & wbit[j]);
-        if (isnew) {
-          const int u = uu[j], ww = w[j];
-          const uint32_t ucol = mcol(L, (uint32_t)u);
-          atomicOr(mw[j], wbit[j]);
-          atomicOr(a.mark + mword(L, (uint32_t)ww, ucol), 1u << (ucol & 31));
-          const float duv = __fsub_rn(__ldg(&tdp[qc[j]]), tdu[j]);
-          a.D[(size_t)u * N + ww] = duv;
-          a.D[(size_t)ww * N + u] = duv;
-          atomicAdd(&a.cnt[ww], 1);
+        for (int j = 0; j < U; j++) {
+          const unsigned k = kb + 32u * j + lane;
+          ew[j] = k < kend ? __ldg(&pre[qb + k]) : 0u;
         }
-        const unsigned nb = __popc(__ballot_sync(0xffffffffu, isnew));
-        if (lane == 0 && nb && uu[j] != s) atomicAdd(&a.cnt[uu[j]], (int)nb);
-        total_new += nb;
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+          const unsigned k = kb + 32u * j + lane;
+          word[j] = k < kend ? __ldcg(mrow + (ew[j] >> 21)) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+          const uint32_t wcol = ew[j] >> 16;
+          if (!((word[j] >> (wcol & 31)) & 1u)) {
+            const int w = (int)(ew[j] & 0xFFFFu);
+            atomicOr(mrow + (wcol >> 5), 1u << (wcol & 31));
+            atomicOr(a.mark + (size_t)w * L.RW + (ucol >> 5), 1u << (ucol & 31));
+            const float duv = __fsub_rn(__ldg(&tdp[qb + kb + 32u * j + lane]), __ldg(&tdp[qb - 1]));
+            a.D[(size_t)u * N + w] = duv;
+            a.D[(size_t)w * N + u] = duv;
+            atomicAdd(&a.cnt[w], 1);
+            unew++;
+          }
+        }
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) unew += __shfl_xor_sync(0xffffffffu, unew, o);
+      if (lane == 0 && unew && u != s) atomicAdd(&a.cnt[u], (int)unew);
+      total_new += unew;
     }
     count -= take;
     q += 32;
@@ -395,7 +391,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
       const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
       if (PU <= nwarps) {  // one unit per warp: static
         const int u = (int)blockIdx.x * (int)(blockDim.x >> 5) + (int)(threadIdx.x >> 5);
-        if (u < PU) lnew = fill_warp_share<G>(a, slot, s, u);
+        if (u < PU) lnew = fill_unit<G>(a, slot, s, u);
       } else {
         int* ctr = &unit_ctr[step & 1];
         int k = lane == 0 ? atomicAdd(ctr, 1) : 0;
@@ -404,7 +400,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
           const int u = (int)blockIdx.x + k * (int)gridDim.x;
           if (u >= PU) break;
           int nk = lane == 0 ? atomicAdd(ctr, 1) : 0;
-          lnew += fill_warp_share<G>(a, slot, s, u);
+          lnew += fill_unit<G>(a, slot, s, u);
           k = __shfl_sync(0xffffffffu, nk, 0);
         }
         if (threadIdx.x == 0) unit_ctr[(step & 1) ^ 1] = 0;  // next step's counter
@@ -482,12 +478,20 @@ int commit_threads() {
   return t;
 }
 
+// G = fill loop unroll (pairs in flight per lane per ancestor): GP_FILL_UNROLL
 static const void* commit_kernel(int G) {
-  (void)G;
-  return (const void*)k_commit<4, 512, 2>;
+  return G >= 4 ? (const void*)k_commit<4, 512, 2>
+       : G == 1 ? (const void*)k_commit<1, 512, 2> : (const void*)k_commit<2, 512, 2>;
 }
 
-int commit_fill_depth() { return 4; }
+int commit_fill_depth() {
+  static int g = 0;
+  if (!g) {
+    g = 2;
+    if (const char* e = getenv("GP_FILL_UNROLL")) g = atoi(e) >= 4 ? 4 : atoi(e) == 1 ? 1 : 2;
+  }
+  return g;
+}
 
 int commit_max_blocks() {
   int dev = 0, nsm = 0, per_sm = 0;

@@ -73,6 +73,8 @@ __host__ __device__ inline MarkLayout make_layout(int N, int H, int W) {
   L.W = W;
   L.tiled = (H >= 16 && W >= 16) ? 1 : 0;
   L.TWn = (W + 15) / 16;
+  // tile columns must fit 16 bits (packed tree-store entries)
+  if (L.tiled && (long long)((H + 15) / 16) * L.TWn * 256 > 65536) L.tiled = 0;
   L.RW = L.tiled ? ((H + 15) / 16) * L.TWn * 8 : (N + 31) / 32;
   L.magic = L.tiled ? (uint32_t)((0x100000000ull / (unsigned long long)W) + 1ull) : 0u;
   return L;

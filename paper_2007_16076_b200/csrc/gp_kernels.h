@@ -10,7 +10,7 @@ namespace gp {
 
 // ---------------- tree store ----------------
 // One committed-or-speculative tree per slot, in Euler-tour (preorder) form:
-//   pre[q]   pixel at preorder position q (u16)
+//   pre[q]   entry at preorder position q: (tile column << 16) | pixel (u32)
 //   szp[q]   number of descendants of pre[q] (u16)
 //   tdp[q]   geodesic distance of pre[q] from the root (fp32)
 //   part[p]  start of commit-warp p's share of the fill work, packed
@@ -19,7 +19,7 @@ namespace gp {
 // desc(pre[q]) = pre[q+1 .. q+szp[q]], so the ancestor/descendant pairs of
 // the tree are the contiguous ranges of this array (no pointer chasing).
 struct TreeStore {
-  uint16_t* pre;
+  uint32_t* pre;
   uint16_t* szp;
   float* tdp;
   uint32_t* part;
@@ -41,6 +41,7 @@ struct PropArgs {
   float* out_dist;         // [slot][N] pixel-order distances (nullable)
   uint8_t* out_dir;        // [slot][N] parent window codes (nullable)
   TreeStore ts;            // Euler-tour outputs (ts.pre == nullptr: none)
+  MarkLayout L;            // mark-bitmap column layout (tile columns in ts.pre)
   uint8_t* scratch;        // per-CTA scratch when the map does not fit smem
   size_t scratch_bytes;
   int in_smem;

@@ -505,10 +505,12 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     szS[q] = szB[v];
   }
   __syncthreads();
-  uint16_t* gpre = a.ts.pre + off;
+  uint32_t* gpre = a.ts.pre + off;
   uint16_t* gszp = a.ts.szp + off;
+  const MarkLayout ML = a.L;
   for (int q = tid; q < N; q += nthr) {
-    gpre[q] = preS[q];
+    const uint32_t v = preS[q];
+    gpre[q] = (mcol(ML, v) << 16) | v;
     gszp[q] = szS[q];
   }
   // E7: chunk counts ceil(szp/32), exclusive scan over preorder, partition
