@@ -39,6 +39,7 @@ struct gp_ctx {
   int isint;
   float* d_img = nullptr;
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;  // propagation stream (overlapped with the commit loop)
   int nsm = 148;
   // tree store (Euler-tour form) + propagation scratch, lazily sized
   TreeStore ts{};
@@ -170,6 +171,7 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
   cudaFree(c->bar);
   cudaFree(c->scratch);
   if (c->st) cudaStreamDestroy(c->st);
+  if (c->st2) cudaStreamDestroy(c->st2);
   delete c;
 }
 
@@ -516,14 +518,13 @@ static int store_relayout(gp_store* s, const MarkLayout& L) {
   return GP_OK;
 }
 
-static int commit_blocks(gp_ctx* c) {
-  if (c->commit_blocks) return c->commit_blocks;
-  int maxb = commit_max_blocks();
-  int bps = 2048 / commit_threads();
+// Commit CTAs: two per SM when the loop has the GPU alone; one per SM when
+// propagation batches run concurrently on the other half of each SM.
+static int commit_blocks(gp_ctx* c, bool overlap) {
+  const int maxb = commit_max_blocks();
+  int bps = overlap ? 1 : 2048 / commit_threads();
   if (const char* e = getenv("GP_COMMIT_BLOCKS_PER_SM")) bps = atoi(e);
-  int nb = std::max(1, std::min(maxb, bps * c->nsm));
-  c->commit_blocks = nb;
-  return nb;
+  return std::max(1, std::min(maxb, bps * c->nsm));
 }
 
 extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, int spec_k,
@@ -590,15 +591,25 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     cudaEventDestroy(pp.a); cudaEventDestroy(pp.b);
   } else {
     // ---- device commit loop with speculative propagation batches ----
-    const int nblocks = commit_blocks(c);
-    // work units per tree = UF x commit warps (dynamic balancing in k_commit)
-    int uf = N >= 32768 ? 4 : 1;
+    // Default: commit launches and propagation batches alternate, each with the
+    // whole GPU.  GP_OVERLAP=1 runs the commit kernel on one CTA per SM and
+    // keeps a second stream producing the trees of the best unclaimed
+    // candidates on the other half of each SM (no kernel ever waits on another:
+    // the commit kernel leaves on a miss, K1 publishes a tree by writing
+    // slot_of[src] after it is complete).  Measured slower on B200 (both roles
+    // are latency/issue-bound and contend), so it is off by default.
+    const bool overlap = getenv("GP_OVERLAP") ? atoi(getenv("GP_OVERLAP")) != 0 : false;
+    const int nblocks = commit_blocks(c, overlap);
+    int uf = N >= 32768 ? 4 : 1;  // work units per commit warp (dynamic balancing)
     if (const char* e = getenv("GP_UNITS_PER_WARP")) uf = std::max(1, atoi(e));
     const int nparts = nblocks * (commit_threads() / 32) * uf;
     int rts = ensure_tree_store(c, nparts);
     if (rts) return rts;
+    if (!c->st2) CUDA_TRY(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    cudaStream_t ps = c->st2;
     int *d_slot_of = nullptr, *d_rank = nullptr, *d_ext = nullptr, *d_cands = nullptr;
-    int *d_slots = nullptr, *d_free = nullptr;
+    int* d_slots = nullptr;
+    uint8_t* d_claimed = nullptr;
     unsigned long long* d_selkey = nullptr;
     Ctl* d_ctl = nullptr;
     float* d_dfc = nullptr;
@@ -611,7 +622,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     CUDA_TRY(cudaMemsetAsync(d_flags, 0, (size_t)(N + 2) * 4, st));
     CUDA_TRY(ws_get(c, WS_CTL, &d_ctl, 1));
     CUDA_TRY(ws_get(c, WS_DFC, &d_dfc, N));
-    CUDA_TRY(ws_get(c, WS_FREE, &d_free, N));
+    CUDA_TRY(ws_get(c, WS_FREE, &d_claimed, N));
     if (!c->bar) CUDA_TRY(dalloc(&c->bar, 1));
     CUDA_TRY(cudaMemsetAsync(c->bar, 0, sizeof(GridBarrier), st));
     {
@@ -620,6 +631,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
       CUDA_TRY(cudaMemcpyAsync(&c->bar->pad0[0], &use_cg, 4, cudaMemcpyHostToDevice, st));
     }
     CUDA_TRY(cudaMemsetAsync(d_slot_of, 0xFF, (size_t)N * 4, st));
+    CUDA_TRY(cudaMemsetAsync(d_claimed, 0, (size_t)N, st));
     CUDA_TRY(cudaMemsetAsync(d_selkey, 0xFF, (size_t)(N + 2) * 8, st));
     Ctl h_ctl;
     memset(&h_ctl, 0, sizeof(h_ctl));
@@ -643,7 +655,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
       if (r) return r;
       std::vector<int32_t> ext, rank(N);
       ext_order(dfc, ext);
-      for (int i = 0; i < N; i++) rank[ext[i]] = i;
+      for (int i2 = 0; i2 < N; i2++) rank[ext[i2]] = i2;
       CUDA_TRY(cudaMemcpyAsync(d_rank, rank.data(), N * 4, cudaMemcpyHostToDevice, st));
       CUDA_TRY(cudaMemcpyAsync(d_ext, ext.data(), N * 4, cudaMemcpyHostToDevice, st));
       S.centroid = cen;
@@ -654,7 +666,9 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     int K = spec_k > 0 ? spec_k : 2 * c->nsm;
     if (spec_k <= 0)
       if (const char* e = getenv("GP_SPEC_K")) K = atoi(e);
-    K = std::min(K, N);
+    K = std::max(1, std::min(K, N));
+    int Q = overlap ? 2 * K : 0;  // lookahead bound of the concurrent batches
+    if (const char* e = getenv("GP_LOOKAHEAD")) Q = atoi(e);
     CUDA_TRY(ws_get(c, WS_CANDS, &d_cands, K));
     CUDA_TRY(ws_get(c, WS_SLOTS, &d_slots, K));
     int rcs = ensure_scratch(c, (size_t)K);
@@ -666,7 +680,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     ca.strategy = strategy == GP_STRATEGY_FILLING_RATE ? kFillingRate : kNaive;
     ca.ts = c->ts;
     ca.slot_of = d_slot_of;
-    ca.free_stack = d_free;
+    ca.claimed = d_claimed;
     ca.mark = s->mark;
     ca.cnt = s->cnt;
     ca.D = s->D;
@@ -679,9 +693,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     ca.ctl = d_ctl;
     ca.max_steps = N + 1;
     ca.bar = c->bar;
-
     ca.total_pairs = ((unsigned long long)N * N - N) / 2;
-
     PropArgs pa = base_prop(c);
     pa.src = d_cands;
     pa.ns = 1;
@@ -689,41 +701,56 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     pa.slot = d_slots;
     pa.ts = c->ts;
     pa.L = L;
+    pa.publish = d_slot_of;
     pa.delta = default_delta(c);
-    // debug phase stamps (GP_DEBUG=1): per tree of the batches, per step
+    pa.threads = overlap ? 512 : 0;
     const bool debug = getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"));
-    unsigned long long *d_pdbg = nullptr, *d_cdbg = nullptr;
-    std::vector<unsigned long long> pdbg_acc(8, 0);
-    long long pdbg_n = 0;
+    unsigned long long* d_cdbg = nullptr;
     if (debug) {
-      CUDA_TRY(dalloc(&d_pdbg, (size_t)K * 8));
       CUDA_TRY(dalloc(&d_cdbg, (size_t)(N + 2) * 6));
       CUDA_TRY(cudaMemsetAsync(d_cdbg, 0, (size_t)(N + 2) * 48, st));
-      pa.dbg = d_pdbg;
       ca.dbg = d_cdbg;
       ca.dbgw = d_cdbg + (size_t)(N + 2) * 4;
     }
     std::vector<EvPair> pev, cev;
-    for (int guard = 0; guard < 4 * N + 8; guard++) {
-      if (debug && guard > 0) {  // fold the previous batch's stamps
-        std::vector<unsigned long long> h((size_t)K * 8);
-        CUDA_TRY(cudaMemcpy(h.data(), d_pdbg, h.size() * 8, cudaMemcpyDeviceToHost));
-        for (int t = 0; t < std::min(K, h_ctl.ncand); t++) {
-          unsigned long long* r = &h[(size_t)t * 8];
-          for (int j = 1; j <= 5; j++) pdbg_acc[j] += r[j] - r[j - 1];
-          pdbg_acc[6] += r[6];
-          pdbg_acc[7] += r[7];
-          pdbg_n++;
-        }
-      }
+    cudaEvent_t ev_c, ev_p;
+    cudaEventCreateWithFlags(&ev_c, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_p, cudaEventDisableTiming);
+    // one propagation batch on the propagation stream (lookahead q)
+    auto batch = [&](int q) -> int {
+      EvPair f;
+      cudaEventCreate(&f.a); cudaEventCreate(&f.b);
+      CUDA_TRY(cudaEventRecord(f.a, ps));
+      CUDA_TRY(launch_topk(ca, K, q, d_cands, d_slots, ps));
+      CUDA_TRY(launch_propagate(pa, K, ps));
+      CUDA_TRY(cudaEventRecord(f.b, ps));
+      CUDA_TRY(cudaEventRecord(ev_p, ps));
+      pev.push_back(f);
+      S.batches++;
+      S.kernels += 2;
+      return GP_OK;
+    };
+    // the first batch must see the initialised workspace on `st`
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (int r = batch(0)) return r;
+    CUDA_TRY(cudaStreamSynchronize(ps));
+    for (int guard = 0; guard < 8 * N + 16; guard++) {
       EvPair e;
       cudaEventCreate(&e.a); cudaEventCreate(&e.b);
       CUDA_TRY(cudaEventRecord(e.a, st));
       CUDA_TRY(launch_commit(ca, nblocks, st));
       CUDA_TRY(cudaEventRecord(e.b, st));
+      CUDA_TRY(cudaEventRecord(ev_c, st));
       cev.push_back(e);
       S.launches++;
       S.kernels++;
+      if (overlap) {  // keep the propagation stream busy while the commit loop runs
+        while (cudaEventQuery(ev_c) == cudaErrorNotReady) {
+          if (cudaEventQuery(ev_p) != cudaErrorNotReady) {
+            if (int r = batch(Q)) return r;
+          }
+        }
+      }
       CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
       if (h_ctl.status == CTL_DONE) break;
@@ -748,16 +775,17 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
         continue;
       }
       if (h_ctl.status != CTL_MISS) { rc = fail(GP_EINTERNAL, "commit loop stopped unexpectedly"); break; }
-      EvPair f;
-      cudaEventCreate(&f.a); cudaEventCreate(&f.b);
-      CUDA_TRY(cudaEventRecord(f.a, st));
-      CUDA_TRY(launch_topk(ca, K, d_cands, d_slots, st));
-      CUDA_TRY(launch_propagate(pa, K, st));
-      CUDA_TRY(cudaEventRecord(f.b, st));
-      pev.push_back(f);
-      S.batches++;
-      S.kernels += 2;
+      // miss: the selected source's tree is in flight (wait) or unclaimed (urgent batch)
+      CUDA_TRY(cudaStreamSynchronize(ps));
+      int sl = -1;
+      CUDA_TRY(cudaMemcpyAsync(&sl, d_slot_of + h_ctl.cur_src, 4, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      if (sl < 0) {
+        if (int r = batch(0)) return r;
+        CUDA_TRY(cudaStreamSynchronize(ps));
+      }
     }
+    CUDA_TRY(cudaStreamSynchronize(ps));
     CUDA_TRY(cudaEventRecord(tot.b, st));
     CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -770,42 +798,21 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
         cudaMemcpy(hw.data(), ca.dbgw, hw.size() * 8, cudaMemcpyDeviceToHost);
         const int nwarps = nblocks * (commit_threads() / 32);
         if (FILE* fp = fopen(path, "w")) {
-          for (int i = 0; i < h_ctl.step; i++) {
-            unsigned long long* r = &h[(size_t)i * 4];
-            fprintf(fp, "%d %llu %llu %llu %llu %llu %llu %llu\n", i, r[0], r[1], r[2], r[3], nw2[i],
-                    hw[(size_t)i * 2], hw[(size_t)i * 2 + 1] / (unsigned long long)nwarps);
+          for (int i2 = 0; i2 < h_ctl.step; i2++) {
+            unsigned long long* r = &h[(size_t)i2 * 4];
+            fprintf(fp, "%d %llu %llu %llu %llu %llu %llu %llu\n", i2, r[0], r[1], r[2], r[3], nw2[i2],
+                    hw[(size_t)i2 * 2], hw[(size_t)i2 * 2 + 1] / (unsigned long long)nwarps);
           }
           fclose(fp);
         }
       }
-      std::vector<double> ph[4];
-      for (int i = 0; i + 1 < h_ctl.step; i++) {
-        unsigned long long* r = &h[(size_t)i * 4];
-        unsigned long long* r2 = &h[(size_t)(i + 1) * 4];
-        if (!r[0] || !r2[0]) continue;
-        ph[0].push_back(r[1] - r[0]); ph[1].push_back(r[2] - r[1]);
-        ph[2].push_back(r[3] - r[2]); ph[3].push_back(r2[0] - r[3]);
-      }
-      auto med = [](std::vector<double>& v) {
-        if (v.empty()) return 0.0;
-        std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
-        return v[v.size() / 2] / 1e3;
-      };
-      if (!ph[0].empty())
-        fprintf(stderr, "[gp debug] commit per step, median (us): fill(warp0) %.2f +rest-of-fill+barrier %.2f select %.2f barrier+next %.2f (n=%zu)\n",
-                med(ph[0]), med(ph[1]), med(ph[2]), med(ph[3]), ph[0].size());
-      if (pdbg_n)
-        fprintf(stderr, "[gp debug] propagate per tree (us): relax %.1f parents %.1f jump %.1f levels %.1f out %.1f | passes %.1f items/N %.2f (trees=%lld)\n",
-                pdbg_acc[1] / 1e3 / pdbg_n, pdbg_acc[2] / 1e3 / pdbg_n, pdbg_acc[3] / 1e3 / pdbg_n,
-                pdbg_acc[4] / 1e3 / pdbg_n, pdbg_acc[5] / 1e3 / pdbg_n, (double)pdbg_acc[6] / pdbg_n,
-                (double)pdbg_acc[7] / pdbg_n / N, pdbg_n);
-      cudaFree(d_pdbg);
       cudaFree(d_cdbg);
     }
     for (auto& e : cev) { S.ms_commit += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (auto& e : pev) { S.ms_propagate += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    cudaEventDestroy(ev_c);
+    cudaEventDestroy(ev_p);
     P = h_ctl.step;
-
     S.propagations += h_ctl.total_props;
     S.visits = (int64_t)h_ctl.visits;
   }

@@ -350,12 +350,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   unsigned ln = mode ? __ldcg(&a.ctl->list_n[lcur]) : 0u;
   unsigned long long filled = 0, visits = 0;
   unsigned dead = 0;
-  int free_top = 0;
   if (keeper) {
     filled = a.ctl->filled;
     visits = a.ctl->visits;
     dead = a.ctl->list_dead;
-    free_top = a.ctl->free_top;
   }
   int slot = -1;
   if (s == -1) {  // first launch: select the first source
@@ -422,8 +420,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     if (keeper) {
       a.cnt[s] = N - 1;  // the root pairs with every pixel
       a.seq[step] = s;
-      a.slot_of[s] = -2;  // committed: recycle the slot
-      a.free_stack[free_top++] = slot;
+      a.slot_of[s] = -2;  // committed
     }
     // ---- K3: selection of the next source (+ keeper's accounting) ----
     unsigned long long stepnew = 0;
@@ -463,7 +460,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     a.ctl->visits = visits;
     a.ctl->list_dead = dead;
     a.ctl->list_cur = lcur;
-    a.ctl->free_top = free_top;
   }
 }
 
@@ -557,15 +553,19 @@ cudaError_t launch_build_list(const MarkLayout& L, const uint32_t* mark, uint32_
   return cudaGetLastError();
 }
 
-// ---- speculative candidate batch: the K smallest keys among open pixels
-// without a tree (radix select, MSB first, single CTA); assigns tree slots
-// (recycled first) and records slot_of[] ----
-__global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int* cands, int* slots) {
-  __shared__ unsigned hist[256];
-  __shared__ unsigned s_prefix, s_mask, s_k, s_all;
-  __shared__ int s_n;
+// ---- speculative candidate batch (single CTA) ----
+// K-th smallest key among the pixels passing `elig` (radix select, MSB
+// first); returns 0xFFFFFFFE when fewer than K are eligible.
+template <typename Elig>
+__device__ unsigned radix_kth(const CommitArgs& a, unsigned K, Elig elig, unsigned* hist,
+                              unsigned* shv) {
   const int N = a.g.N, tid = threadIdx.x;
-  if (tid == 0) { s_prefix = 0; s_mask = 0; s_k = (unsigned)K; s_all = 0; s_n = 0; }
+  unsigned& s_prefix = shv[0];
+  unsigned& s_mask = shv[1];
+  unsigned& s_k = shv[2];
+  unsigned& s_all = shv[3];
+  if (tid == 0) { s_prefix = 0; s_mask = 0; s_k = K; s_all = 0; }
+  __syncthreads();
   for (int pass = 0; pass < 4; pass++) {
     const int shift = 24 - 8 * pass;
     for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
@@ -573,9 +573,8 @@ __global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int* cands, 
     const unsigned prefix = s_prefix, mask = s_mask;
     if (!s_all) {
       for (int v = tid; v < N; v += blockDim.x) {
-        if (__ldcg(&a.slot_of[v]) != -1) continue;
-        unsigned key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
-        if (key == 0xFFFFFFFFu || (key & mask) != prefix) continue;
+        unsigned key;
+        if (!elig(v, key) || (key & mask) != prefix) continue;
         atomicAdd(&hist[(key >> shift) & 255u], 1u);
       }
     }
@@ -601,10 +600,37 @@ __global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int* cands, 
     __syncthreads();
   }
   const unsigned thr = s_all ? 0xFFFFFFFEu : s_prefix;
+  __syncthreads();
+  return thr;
+}
+
+// Candidates: the K smallest keys among open, unclaimed pixels, restricted to
+// the Q smallest keys among all open pixels (lookahead bound; Q = 0: none).
+// Claims them and hands out tree slots (bump allocator: a pixel is propagated
+// at most once, so N slots always suffice).  The tree becomes visible to the
+// commit loop only when K1 publishes slot_of[src] after writing it.
+__global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int Q, int* cands, int* slots) {
+  __shared__ unsigned hist[256];
+  __shared__ unsigned shv[4];
+  __shared__ int s_n;
+  const int N = a.g.N, tid = threadIdx.x;
+  if (tid == 0) s_n = 0;
+  unsigned lim = 0xFFFFFFFEu;
+  if (Q > 0) {
+    lim = radix_kth(a, (unsigned)Q, [&](int v, unsigned& key) {
+      key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
+      return key != 0xFFFFFFFFu;
+    }, hist, shv);
+  }
+  auto unclaimed = [&](int v, unsigned& key) {
+    if (__ldcg(&a.claimed[v])) return false;
+    key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
+    return key != 0xFFFFFFFFu && key <= lim;
+  };
+  const unsigned thr = radix_kth(a, (unsigned)K, unclaimed, hist, shv);
   for (int v = tid; v < N; v += blockDim.x) {
-    if (__ldcg(&a.slot_of[v]) != -1) continue;
-    unsigned key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
-    if (key == 0xFFFFFFFFu || key > thr) continue;
+    unsigned key;
+    if (!unclaimed(v, key) || key > thr) continue;
     int i = atomicAdd(&s_n, 1);
     if (i < K) cands[i] = v;
   }
@@ -613,17 +639,17 @@ __global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int* cands, 
     const int n = min(s_n, K);
     Ctl* c = a.ctl;
     for (int i = 0; i < n; i++) {
-      int sl = c->free_top > 0 ? a.free_stack[--c->free_top] : c->nslots++;
-      slots[i] = sl;
-      a.slot_of[cands[i]] = sl;
+      slots[i] = c->nslots++;
+      a.claimed[cands[i]] = 1;
     }
     c->ncand = n;
     c->total_props += n;
   }
 }
 
-cudaError_t launch_topk(const CommitArgs& a, int K, int* cands, int* slots, cudaStream_t st) {
-  k_topk<<<1, 1024, 0, st>>>(a, K, cands, slots);
+cudaError_t launch_topk(const CommitArgs& a, int K, int Q, int* cands, int* slots,
+                        cudaStream_t st) {
+  k_topk<<<1, 1024, 0, st>>>(a, K, Q, cands, slots);
   return cudaGetLastError();
 }
 

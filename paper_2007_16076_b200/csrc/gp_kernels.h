@@ -48,6 +48,8 @@ struct PropArgs {
   float delta;             // bucket width (inf = plain frontier relaxation)
   float* D;                // naive epilogue: D row/col x > src (nullable)
   unsigned long long* dbg; // optional per-tree phase stamps [ntrees][8] (debug)
+  int* publish;            // optional slot_of[]: set slot_of[src] = slot once the tree is written
+  int threads;             // CTA size override (0: automatic)
 };
 
 size_t prop_smem_bytes(int N);
@@ -62,7 +64,7 @@ struct Ctl {
   int status;     // CTL_*
   int nslots;     // slots ever handed out (bump allocator)
   int ncand;      // candidates produced by the last top-K
-  int free_top;   // free-slot stack height
+  int pad2;
   int total_props; // trees propagated by speculative batches
   int mode;        // 0: Euler-range fill, 1: unfilled-pair list fill
   unsigned long long visits;  // sum of C over committed trees
@@ -87,8 +89,8 @@ struct CommitArgs {
   MarkLayout L;
   int strategy;            // kNaive (naive_with_tree) or kFillingRate
   TreeStore ts;
-  int* slot_of;            // [N] slot of a pixel's tree, -1 none, -2 committed
-  int* free_stack;         // [cap] recycled slots
+  int* slot_of;            // [N] slot of a pixel's tree, -1 none (or in flight), -2 committed
+  uint8_t* claimed;        // [N] 1 once a pixel is handed to a propagation batch
   uint32_t* mark;          // [N][RW] bitmap
   int* cnt;                // [N] marked off-diagonal entries per pixel
   float* D;                // [N][N]
@@ -112,7 +114,8 @@ constexpr uint32_t LIST_DEAD = 0xFFFFFFFFu;
 cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st);
 int commit_max_blocks();
 int commit_fill_depth();
-cudaError_t launch_topk(const CommitArgs& a, int K, int* cands, int* slots, cudaStream_t st);
+cudaError_t launch_topk(const CommitArgs& a, int K, int Q, int* cands, int* slots,
+                        cudaStream_t st);
 
 // ---------------- store helpers ----------------
 cudaError_t launch_store_init(const MarkLayout& L, uint32_t* mark, float* D, cudaStream_t st);

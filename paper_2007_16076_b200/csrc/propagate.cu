@@ -599,6 +599,11 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     __syncthreads();
     if (tid == 0) dbg[5] = gtimer();
   }
+  if (a.publish) {  // the tree is complete: make it visible to the commit loop
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicExch(&a.publish[my_src[0]], slot);
+  }
 }
 
 size_t prop_smem_bytes(int N) { return prop_layout(N, HIST_SMEM).total; }
@@ -629,6 +634,7 @@ cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st) {
   // 2 x 512 x <=64); 128x128 maps need ~212 KB and keep 1024 threads.
   const size_t per_cta = smem + 1024 + sizeof(PropShared);
   int threads = (228 * 1024) / per_cta >= 2 ? 512 : 1024;
+  if (a.threads) threads = a.threads;
   if (const char* e = getenv("GP_PROP_THREADS")) threads = std::max(128, std::min(1024, atoi(e)));
   k_propagate<<<ntrees, threads, smem, st>>>(a);
   return cudaGetLastError();
