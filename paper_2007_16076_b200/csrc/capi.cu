@@ -706,7 +706,26 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     pa.threads = overlap ? 512 : 0;
     const bool debug = getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"));
     unsigned long long* d_cdbg = nullptr;
+    unsigned long long* d_pdbg = nullptr;
+    std::vector<double> pacc(8, 0.0);
+    long long pn = 0;
+    auto fold_pdbg = [&]() {  // per-tree phase stamps of the last (completed) batch
+      if (!d_pdbg) return;
+      int nc = 0;
+      cudaMemcpy(&nc, &d_ctl->ncand, 4, cudaMemcpyDeviceToHost);
+      std::vector<unsigned long long> h((size_t)K * 8);
+      cudaMemcpy(h.data(), d_pdbg, h.size() * 8, cudaMemcpyDeviceToHost);
+      for (int t = 0; t < std::min(nc, K); t++) {
+        const unsigned long long* r = &h[(size_t)t * 8];
+        for (int j = 1; j <= 5; j++) pacc[j] += (double)(r[j] - r[j - 1]);
+        pacc[6] += (double)r[6];
+        pacc[7] += (double)r[7];
+        pn++;
+      }
+    };
     if (debug) {
+      CUDA_TRY(dalloc(&d_pdbg, (size_t)K * 8));
+      pa.dbg = d_pdbg;
       CUDA_TRY(dalloc(&d_cdbg, (size_t)(N + 2) * 6));
       CUDA_TRY(cudaMemsetAsync(d_cdbg, 0, (size_t)(N + 2) * 48, st));
       ca.dbg = d_cdbg;
@@ -734,6 +753,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     CUDA_TRY(cudaStreamSynchronize(st));
     if (int r = batch(0)) return r;
     CUDA_TRY(cudaStreamSynchronize(ps));
+    fold_pdbg();
     for (int guard = 0; guard < 8 * N + 16; guard++) {
       EvPair e;
       cudaEventCreate(&e.a); cudaEventCreate(&e.b);
@@ -783,6 +803,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
       if (sl < 0) {
         if (int r = batch(0)) return r;
         CUDA_TRY(cudaStreamSynchronize(ps));
+        fold_pdbg();
       }
     }
     CUDA_TRY(cudaStreamSynchronize(ps));
@@ -807,6 +828,11 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
         }
       }
       cudaFree(d_cdbg);
+      if (pn)
+        fprintf(stderr, "[gp debug] propagate per tree (us): relax %.1f parents %.1f jump %.1f levels %.1f out %.1f | passes %.1f items/N %.2f (trees=%lld)\n",
+                pacc[1] / 1e3 / pn, pacc[2] / 1e3 / pn, pacc[3] / 1e3 / pn, pacc[4] / 1e3 / pn,
+                pacc[5] / 1e3 / pn, pacc[6] / pn, pacc[7] / pn / N, pn);
+      cudaFree(d_pdbg);
     }
     for (auto& e : cev) { S.ms_commit += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (auto& e : pev) { S.ms_propagate += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }

@@ -133,6 +133,37 @@ __device__ void pointer_jump(volatile uint32_t* pj, int N) {
   }
 }
 
+// global-scratch variant: the same with L2 loads (__ldcg, no stale L1) and four
+// independent chains per thread in flight
+__device__ void pointer_jump_global(uint32_t* pj, int N) {
+  for (;;) {
+    int ch = 0;
+    for (int v0 = threadIdx.x; v0 < N; v0 += 4 * blockDim.x) {
+      uint32_t pr[4], px[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int v = v0 + j * blockDim.x;
+        pr[j] = v < N ? __ldcg(&pj[v]) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int v = v0 + j * blockDim.x;
+        px[j] = v < N ? __ldcg(&pj[pr[j] & 0xFFFFu]) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int v = v0 + j * blockDim.x;
+        const uint32_t jj = px[j] & 0xFFFFu;
+        if (v < N && jj != (pr[j] & 0xFFFFu)) {
+          __stcg(&pj[v], ((pr[j] & 0xFFFF0000u) + (px[j] & 0xFFFF0000u)) | jj);
+          ch = 1;
+        }
+      }
+    }
+    if (!__syncthreads_or(ch)) break;
+  }
+}
+
 __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   const Grid g = a.g;
   const int N = g.N, NW = (N + 31) >> 5;
@@ -144,7 +175,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   unsigned long long* dbg = a.dbg ? a.dbg + (size_t)t * 8 : nullptr;
   if (dbg && tid == 0) dbg[0] = gtimer();
 
-  const size_t hist_cap = a.in_smem ? HIST_SMEM : (size_t)N + 1;
+  const size_t hist_cap = HIST_SMEM;
   const Layout lay = prop_layout(N, hist_cap);
   unsigned char* base = a.in_smem ? g_smem : a.scratch + (size_t)t * a.scratch_bytes;
   uint32_t* dist = reinterpret_cast<uint32_t*>(base);
@@ -161,13 +192,17 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     wl.s[1] = wl.g[1];
     wl.cap = N;
   } else {
-    // global-scratch variant: bitmaps and the head of both worklists in smem
+    // global-scratch variant: bitmaps and the head of both worklists in smem;
+    // after the relaxation the worklist area holds the parent codes and the
+    // depth histogram (the Euler tour's latency-critical arrays)
     const size_t bm = align16((size_t)NW * 4);
     far = reinterpret_cast<uint32_t*>(g_smem);
     inq = reinterpret_cast<uint32_t*>(g_smem + bm);
     wl.s[0] = reinterpret_cast<uint16_t*>(g_smem + 2 * bm);
     wl.s[1] = wl.s[0] + WL_SMEM;
     wl.cap = WL_SMEM;
+    code = g_smem + 2 * bm;
+    hist = reinterpret_cast<uint32_t*>(g_smem + 2 * bm + align16((size_t)N));
   }
   const float* f = a.in_smem ? fimg : a.img;
   if (a.in_smem)
@@ -379,7 +414,8 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     pj[v] = cv == GP_ROOT ? (uint32_t)v : ((1u << 16) | (uint32_t)parent_of(v, cv, g.W));
   }
   __syncthreads();
-  pointer_jump(pj, N);
+  if (a.in_smem) pointer_jump(pj, N);
+  else pointer_jump_global(const_cast<uint32_t*>(pj), N);
   if (dbg && tid == 0) dbg[3] = gtimer();
   // E2: depth (B) and max depth
   volatile uint16_t* depth = reinterpret_cast<volatile uint16_t*>(base + lay.B);
@@ -485,7 +521,8 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     pj[v] = ((1u + offs) << 16) | (uint32_t)pp;
   }
   __syncthreads();
-  pointer_jump(pj, N);
+  if (a.in_smem) pointer_jump(pj, N);
+  else pointer_jump_global(const_cast<uint32_t*>(pj), N);
   if (dbg && tid == 0) dbg[4] = gtimer();
   // E6: preorder arrays.  tdp straight to global, then pre/szp staged in the
   // (now free) distance region for coalesced stores and the partition scan.
@@ -624,7 +661,8 @@ cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st) {
   } else {
     a.scratch_bytes = prop_scratch_bytes(a.g.N);
     const int NW = (a.g.N + 31) >> 5;
-    smem = 2 * align16((size_t)NW * 4) + 2 * (size_t)WL_SMEM * 2;
+    smem = 2 * align16((size_t)NW * 4) +
+           std::max((size_t)WL_SMEM * 4, align16((size_t)a.g.N) + (size_t)HIST_SMEM * 4);
     cudaError_t e = cudaFuncSetAttribute(k_propagate, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
