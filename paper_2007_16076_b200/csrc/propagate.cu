@@ -315,7 +315,9 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
           if (u >= 0) {
             const float nd = __fadd_rn(__uint_as_float(vdist[v]), edge_w(g.metric, f[v], f[u]));
             const uint32_t nb = __float_as_uint(nd);
-            if (nb < vdist[u]) {
+            // pre-check (cheap in smem); in the global variant the atomic's
+            // returned value is the check, saving a dependent L2 round trip
+            if (!a.in_smem || nb < vdist[u]) {
               const uint32_t old = atomicMin(&dist[u], nb);
               if (nb < old) {
                 const uint32_t ub = 1u << (u & 31);
@@ -526,29 +528,39 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   if (dbg && tid == 0) dbg[4] = gtimer();
   // E6: preorder arrays.  tdp straight to global, then pre/szp staged in the
   // (now free) distance region for coalesced stores and the partition scan.
+  // The arrays read here are stable after the barriers: the global variant
+  // reads them from L2 (__ldcg: no stale L1, loads pipeline), smem directly.
+  const bool gm = !a.in_smem;
+  auto rd32 = [gm](const volatile uint32_t* p) -> uint32_t {
+    return gm ? __ldcg(const_cast<const uint32_t*>(p)) : *p;
+  };
+  auto rd16 = [gm](const volatile uint16_t* p) -> uint16_t {
+    return gm ? __ldcg(const_cast<const unsigned short*>(p)) : *p;
+  };
   float* gtdp = a.ts.tdp + off;
   uint16_t* gtin = a.ts.tin + off;
   for (int v = tid; v < N; v += nthr) {
-    const uint32_t q = pj[v] >> 16;
-    gtdp[q] = __uint_as_float(vdist[v]);
+    const uint32_t q = rd32(&pj[v]) >> 16;
+    gtdp[q] = __uint_as_float(rd32(&vdist[v]));
     gtin[v] = (uint16_t)q;
   }
   __syncthreads();
   volatile uint16_t* preS = reinterpret_cast<volatile uint16_t*>(base);
   volatile uint16_t* szS = preS + N;
   for (int v = tid; v < N; v += nthr) {
-    const unsigned q = pj[v] >> 16;
+    const unsigned q = rd32(&pj[v]) >> 16;
+    const uint16_t sz = rd16(&szB[v]);
     preS[q] = (uint16_t)v;
-    szS[q] = szB[v];
+    szS[q] = sz;
   }
   __syncthreads();
   uint32_t* gpre = a.ts.pre + off;
   uint16_t* gszp = a.ts.szp + off;
   const MarkLayout ML = a.L;
   for (int q = tid; q < N; q += nthr) {
-    const uint32_t v = preS[q];
+    const uint32_t v = rd16(&preS[q]);
     gpre[q] = (mcol(ML, v) << 16) | v;
-    gszp[q] = szS[q];
+    gszp[q] = rd16(&szS[q]);
   }
   // E7: chunk counts ceil(szp/32), exclusive scan over preorder, partition
   const int seg = (N + nthr - 1) / nthr;
@@ -557,8 +569,9 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   // the root (q = 0) pairs with every pixel; the commit kernel fills its row
   // with a grid-wide row scan, so its chunks are left out of the partition
   for (int q = q0; q < q1; q++) {
-    lsum += q ? ((unsigned)szS[q] + 31u) >> 5 : 0u;
-    lpairs += szS[q];
+    const unsigned sq = rd16(&szS[q]);
+    lsum += q ? (sq + 31u) >> 5 : 0u;
+    lpairs += sq;
   }
   atomicAdd(&sh.pairs, lpairs);
   unsigned incl = lsum;
@@ -610,7 +623,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   if (tid == 0) sh.nbig = 0;
   __syncthreads();
   for (int q = q0; q < q1; q++) {
-    const unsigned nch = q ? ((unsigned)szS[q] + 31u) >> 5 : 0u;
+    const unsigned nch = q ? ((unsigned)rd16(&szS[q]) + 31u) >> 5 : 0u;
     if (!nch) continue;
     // partitions p whose first chunk floor(p*T/P) lies in [run, run+nch)
     const unsigned long long plo = first_part(run), phi = min(first_part(run + nch), P);
