@@ -675,6 +675,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     if (rcs) return rcs;
     CommitArgs ca;
     memset(&ca, 0, sizeof(ca));
+    ca.fillq = getenv("GP_FILL_QUEUE") ? atoi(getenv("GP_FILL_QUEUE")) != 0 : 1;
     ca.g = c->g;
     ca.L = L;
     ca.strategy = strategy == GP_STRATEGY_FILLING_RATE ? kFillingRate : kNaive;
@@ -707,29 +708,40 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     const bool debug = getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"));
     unsigned long long* d_cdbg = nullptr;
     unsigned long long* d_pdbg = nullptr;
-    std::vector<double> pacc(8, 0.0);
+    std::vector<double> pacc(16, 0.0);
     long long pn = 0;
     auto fold_pdbg = [&]() {  // per-tree phase stamps of the last (completed) batch
       if (!d_pdbg) return;
       int nc = 0;
       cudaMemcpy(&nc, &d_ctl->ncand, 4, cudaMemcpyDeviceToHost);
-      std::vector<unsigned long long> h((size_t)K * 8);
+      std::vector<unsigned long long> h((size_t)K * 16);
       cudaMemcpy(h.data(), d_pdbg, h.size() * 8, cudaMemcpyDeviceToHost);
       for (int t = 0; t < std::min(nc, K); t++) {
-        const unsigned long long* r = &h[(size_t)t * 8];
+        const unsigned long long* r = &h[(size_t)t * 16];
         for (int j = 1; j <= 5; j++) pacc[j] += (double)(r[j] - r[j - 1]);
         pacc[6] += (double)r[6];
         pacc[7] += (double)r[7];
+        pacc[8] += (double)(r[8] - r[3]);
+        pacc[9] += (double)(r[9] - r[8]);
+        pacc[10] += (double)(r[10] - r[9]);
+        pacc[11] += (double)(r[4] - r[10]);
+        pacc[12] += (double)r[11];
         pn++;
       }
     };
     if (debug) {
-      CUDA_TRY(dalloc(&d_pdbg, (size_t)K * 8));
+      CUDA_TRY(dalloc(&d_pdbg, (size_t)K * 16));
       pa.dbg = d_pdbg;
-      CUDA_TRY(dalloc(&d_cdbg, (size_t)(N + 2) * 6));
-      CUDA_TRY(cudaMemsetAsync(d_cdbg, 0, (size_t)(N + 2) * 48, st));
+      CUDA_TRY(dalloc(&d_cdbg, (size_t)(N + 2) * 16));
+      CUDA_TRY(cudaMemsetAsync(d_cdbg, 0, (size_t)(N + 2) * 128, st));
       ca.dbg = d_cdbg;
       ca.dbgw = d_cdbg + (size_t)(N + 2) * 4;
+      if (getenv("GP_DEBUG_SIM")) ca.dbgs = d_cdbg + (size_t)(N + 2) * 8;
+      if (const char* e = getenv("GP_DEBUG_UNITS")) {
+        ca.dbgu_step = atoi(e);
+        CUDA_TRY(dalloc(&ca.dbgu, (size_t)nparts * 8));
+        CUDA_TRY(cudaMemsetAsync(ca.dbgu, 0, (size_t)nparts * 32, st));
+      }
     }
     std::vector<EvPair> pev, cev;
     cudaEvent_t ev_c, ev_p;
@@ -814,24 +826,44 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
       std::vector<unsigned long long> h((size_t)(N + 2) * 4);
       CUDA_TRY(cudaMemcpy(h.data(), d_cdbg, h.size() * 8, cudaMemcpyDeviceToHost));
       if (const char* path = getenv("GP_DEBUG_DUMP")) {  // per-step stamps + new pairs
-        std::vector<unsigned long long> nw2(h_ctl.step), hw((size_t)(N + 2) * 2);
+        std::vector<unsigned long long> nw2(h_ctl.step), hw((size_t)(N + 2) * 4);
         cudaMemcpy(nw2.data(), d_new, (size_t)h_ctl.step * 8, cudaMemcpyDeviceToHost);
         cudaMemcpy(hw.data(), ca.dbgw, hw.size() * 8, cudaMemcpyDeviceToHost);
+        std::vector<unsigned long long> hs((size_t)(N + 2) * 8, 0);
+        if (ca.dbgs) cudaMemcpy(hs.data(), ca.dbgs, hs.size() * 8, cudaMemcpyDeviceToHost);
         const int nwarps = nblocks * (commit_threads() / 32);
         if (FILE* fp = fopen(path, "w")) {
           for (int i2 = 0; i2 < h_ctl.step; i2++) {
             unsigned long long* r = &h[(size_t)i2 * 4];
-            fprintf(fp, "%d %llu %llu %llu %llu %llu %llu %llu\n", i2, r[0], r[1], r[2], r[3], nw2[i2],
-                    hw[(size_t)i2 * 2], hw[(size_t)i2 * 2 + 1] / (unsigned long long)nwarps);
+            const unsigned long long* q = &hs[(size_t)i2 * 8];
+            fprintf(fp, "%d %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i2,
+                    r[0], r[1], r[2], r[3], nw2[i2], hw[(size_t)i2 * 4], hw[(size_t)i2 * 4 + 1] / (unsigned long long)nwarps,
+                    q[0], q[1], q[2], q[3], hw[(size_t)i2 * 4 + 2], hw[(size_t)i2 * 4 + 3] / (unsigned long long)nblocks,
+                    q[4], q[5], q[6], q[7]);
           }
           fclose(fp);
         }
+      }
+      if (ca.dbgu) {
+        std::vector<unsigned> hu((size_t)nparts * 8);
+        cudaMemcpy(hu.data(), ca.dbgu, hu.size() * 4, cudaMemcpyDeviceToHost);
+        if (FILE* fp = fopen(getenv("GP_DEBUG_UNITS_OUT") ? getenv("GP_DEBUG_UNITS_OUT") : "units.txt", "w")) {
+          for (int u = 0; u < nparts; u++) {
+            for (int j = 0; j < 8; j++) fprintf(fp, "%u ", hu[(size_t)u * 8 + j]);
+            fprintf(fp, "\n");
+          }
+          fclose(fp);
+        }
+        cudaFree(ca.dbgu);
       }
       cudaFree(d_cdbg);
       if (pn)
         fprintf(stderr, "[gp debug] propagate per tree (us): relax %.1f parents %.1f jump %.1f levels %.1f out %.1f | passes %.1f items/N %.2f (trees=%lld)\n",
                 pacc[1] / 1e3 / pn, pacc[2] / 1e3 / pn, pacc[3] / 1e3 / pn, pacc[4] / 1e3 / pn,
                 pacc[5] / 1e3 / pn, pacc[6] / pn, pacc[7] / pn / N, pn);
+      if (pn)
+        fprintf(stderr, "[gp debug] levels split (us): depth %.1f sort %.1f sizes %.1f preorder %.1f | mean maxdepth %.1f\n",
+                pacc[8] / 1e3 / pn, pacc[9] / 1e3 / pn, pacc[10] / 1e3 / pn, pacc[11] / 1e3 / pn, pacc[12] / pn);
       cudaFree(d_pdbg);
     }
     for (auto& e : cev) { S.ms_commit += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }

@@ -7,14 +7,19 @@
 //   fill   (K2)  fill_tree_pairs (reference _kernels.py:82-116) over the
 //                tree's Euler tour: the pairs of the tree are
 //                {(pre[q], pre[q+1+k]) : k < szp[q]}, split into 32-pair
-//                chunks and pre-partitioned evenly over every warp of the grid
-//                (propagate.cu E7).  A warp takes one chunk at a time: all 32
-//                lanes share the ancestor u, so their mark bits lie in row u
-//                at the (tile-ordered) columns of one subtree region.  An
-//                unmarked pair sets both bits, writes D[u][w] = D[w][u] =
+//                chunks and pre-partitioned into equal work units
+//                (propagate.cu E7), interleaved over the CTAs.  Each CTA
+//                expands its units' open ancestors into chunk descriptors in
+//                a shared-memory queue, then all its warps drain the queue G
+//                chunks at a time (fill_tree_cta).  The 32 lanes of a chunk
+//                share the ancestor u, so their mark bits lie in row u at the
+//                (tile-ordered) columns of one subtree region.  An unmarked
+//                pair sets both bits, writes D[u][w] = D[w][u] =
 //                fl(td[w] - td[u]) and bumps both counts -- first writer in
 //                commit order, exactly as the reference.  Ancestors whose row
 //                is full (count N-1) are skipped: every bit is already set.
+//                Late in the run the step tests the list of unfilled pairs
+//                instead (fill_list, Euler-interval test).
 //   grid barrier
 //   select (K3)  grid-wide argmin of the packed key (count << 16 | rank) over
 //                open pixels -- FillingRateSelector.next_source
@@ -99,6 +104,19 @@ __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned lo
   if (threadIdx.x == 0 && m != ~0ull) atomicMin(&a.selkey[step], m);
 }
 
+// Mark-word loads of the tree fill may hit L1.  Every grid barrier ends with
+// an L1 invalidation (fence + CCTL.IVALL, both barrier variants), so a cached
+// word holds at least every bit set before the step.  Bits set during the
+// step belong to pairs of the committed tree, and each such pair -- with its
+// mirror bit -- is tested and set by exactly one lane (an ancestor pair occurs
+// once in a tree), so a word cached within the step never hides a bit that
+// lane is about to test.  Neighbouring chunks of one ancestor share lines.
+__device__ __forceinline__ uint32_t ld_mark(const uint32_t* p) { return __ldca(p); }
+
+__device__ __forceinline__ void set_mark(const CommitArgs& a, int row, uint32_t col) {
+  atomicOr(a.mark + (size_t)row * a.L.RW + (col >> 5), 1u << (col & 31));
+}
+
 // K2 for one committed tree: one work unit = chunks [b0, b1) of the tree's
 // chunk sequence (32 consecutive descendants of one preorder position).
 // The warp scans 32 preorder positions at a time (descendant counts, packed
@@ -108,7 +126,8 @@ __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned lo
 // iterations in flight.  The fill is instruction-issue bound, so the loop is
 // kept to a handful of instructions per tested pair.
 template <int U>
-__device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int s, int p) {
+__device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int s, int p,
+                                          unsigned long long* sim = nullptr, unsigned* ustat = nullptr) {
   const int N = a.g.N;
   const int lane = threadIdx.x & 31;
   const int P = a.ts.nparts;
@@ -126,7 +145,9 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
   unsigned coff = pw >> 16;
   unsigned total_new = 0;
   const MarkLayout L = a.L;
+  unsigned n_win = 0, n_own = 0;
   while (count) {
+    n_win++;
     const int qa = q + lane;
     unsigned sz_l = 0;
     uint32_t e_l = 0;
@@ -152,6 +173,7 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
     while (work) {
       const int ol = __ffs(work) - 1;
       work &= work - 1;
+      n_own++;
       const uint32_t eu = __shfl_sync(0xffffffffu, e_l, ol);
       const unsigned sz = __shfl_sync(0xffffffffu, sz_l, ol);
       const unsigned c0 = __shfl_sync(0xffffffffu, c0_l, ol);
@@ -160,6 +182,15 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
       const uint32_t ucol = eu >> 16;
       uint32_t* mrow = a.mark + (size_t)u * L.RW;
       const int qb = q + ol + 1;  // preorder position of the first descendant
+      if (sim && c0 == 0 && lane == 0) {  // debug: per-row list-mode cost model
+        const unsigned ch = (sz + 31u) >> 5;
+        const unsigned unf = (unsigned)(N - 1 - __ldcg(&a.cnt[u]));
+        const unsigned lch = (unf + 31u) >> 5;
+        atomicAdd(&sim[0], (unsigned long long)ch);
+        atomicAdd(&sim[1], (unsigned long long)(unf <= 128u ? min(ch, lch) : ch));
+        atomicAdd(&sim[2], (unsigned long long)(unf <= 1024u ? min(ch, lch) : ch));
+        atomicAdd(&sim[3], (unsigned long long)min(ch, lch));
+      }
       const unsigned kend = min(sz, (c0 + nc) * 32u);
       unsigned unew = 0;
       for (unsigned kb = c0 * 32u; kb < kend; kb += 32u * U) {  // warp-uniform trips
@@ -172,15 +203,15 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
 #pragma unroll
         for (int j = 0; j < U; j++) {
           const unsigned k = kb + 32u * j + lane;
-          word[j] = k < kend ? __ldcg(mrow + (ew[j] >> 21)) : 0xFFFFFFFFu;
+          word[j] = k < kend ? ld_mark(mrow + (ew[j] >> 21)) : 0xFFFFFFFFu;
         }
 #pragma unroll
         for (int j = 0; j < U; j++) {
           const uint32_t wcol = ew[j] >> 16;
           if (!((word[j] >> (wcol & 31)) & 1u)) {
             const int w = (int)(ew[j] & 0xFFFFu);
-            atomicOr(mrow + (wcol >> 5), 1u << (wcol & 31));
-            atomicOr(a.mark + (size_t)w * L.RW + (ucol >> 5), 1u << (ucol & 31));
+            set_mark(a, u, wcol);
+            set_mark(a, w, ucol);
             const float duv = __fsub_rn(__ldg(&tdp[qb + kb + 32u * j + lane]), __ldg(&tdp[qb - 1]));
             a.D[(size_t)u * N + w] = duv;
             a.D[(size_t)w * N + u] = duv;
@@ -198,7 +229,277 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
     q += 32;
     coff = 0;
   }
+  if (ustat && lane == 0) {
+    ustat[1] = n_win;
+    ustat[2] = n_own;
+    ustat[3] = total_new;
+    ustat[4] = b1 - b0;
+  }
   return lane == 0 ? total_new : 0u;
+}
+
+// K2, CTA-queue form (tree mode, default).  The unit-per-warp loop above is
+// latency bound: every unit starts with a dependent chain (partition word ->
+// preorder window -> row counts) and every ancestor with another (entries ->
+// mark words), so warps spend most of a step waiting and finish unevenly.
+// Here a step runs in two phases per CTA:
+//   A  each warp loads the headers and first preorder windows of up to four of
+//      the CTA's units at once and expands their open ancestors into 32-pair
+//      chunk descriptors in a shared-memory queue (one round of each chain per
+//      four units);
+//   B  all warps of the CTA drain the queue G descriptors at a time, chunks of
+//      different ancestors in flight together.
+// A unit that does not fit the queue's remaining room is filled in place by
+// fill_unit (deep trees).  Descriptor: x = pre entry of the ancestor u
+// (tile column << 16 | u); y = qb | chunk << 16 | (valid lanes - 1) << 27,
+// qb = preorder position of u's first descendant.
+constexpr int FQ_CAP = 4096;
+struct FillQ {
+  uint2 desc[FQ_CAP];
+  int n, res, head;
+};
+
+// Chunks of the unit that lie in the 32-position window at q (count left,
+// first owner's chunk offset coff): returns take, sets the lane's share.
+__device__ __forceinline__ unsigned fq_window(int lane, int qa, unsigned sz_l, unsigned coff,
+                                              unsigned count, unsigned& mych, unsigned& c0_l) {
+  unsigned nch_l = qa ? (sz_l + 31u) >> 5 : 0u;  // root row: see fill_root_row
+  c0_l = 0;
+  if (lane == 0) { nch_l -= coff; c0_l = coff; }
+  unsigned cum = nch_l;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, cum, o);
+    if (lane >= o) cum += y;
+  }
+  const unsigned take = min(__shfl_sync(0xffffffffu, cum, 31), count);
+  const unsigned excl = cum - nch_l;
+  mych = excl < take ? min(nch_l, take - excl) : 0u;
+  return take;
+}
+
+// Chunk descriptors of the open owners of a window at q: `incl` = inclusive
+// scan of the open owners' chunk counts (returns the window total); fq_write
+// stores descriptors [base, base + total), 32 per warp pass, each lane finding
+// its owner by binary search over the scan.
+__device__ __forceinline__ unsigned fq_scan(int lane, unsigned nop, unsigned& incl) {
+  incl = nop;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+__device__ __forceinline__ void fq_write(FillQ& Q, int lane, unsigned base, unsigned total,
+                                         unsigned incl, unsigned nop, int q, uint32_t e_l,
+                                         unsigned sz_l, unsigned c0_l) {
+  const unsigned excl = incl - nop;
+  for (unsigned i0 = 0; i0 < total; i0 += 32) {
+    const unsigned idx = i0 + lane;
+    int ol = 0;  // lanes with incl <= idx = the owner of descriptor idx
+#pragma unroll
+    for (int b = 16; b; b >>= 1)
+      if (__shfl_sync(0xffffffffu, incl, ol + b - 1) <= idx) ol += b;
+    const unsigned ex = __shfl_sync(0xffffffffu, excl, ol);
+    const uint32_t eu = __shfl_sync(0xffffffffu, e_l, ol);
+    const unsigned sz = __shfl_sync(0xffffffffu, sz_l, ol);
+    const unsigned c0 = __shfl_sync(0xffffffffu, c0_l, ol);
+    if (idx < total) {
+      const unsigned c = c0 + (idx - ex);
+      const unsigned nv = min(32u, sz - c * 32u);
+      Q.desc[base + idx] = make_uint2(eu, (unsigned)(q + ol + 1) | (c << 16) | ((nv - 1u) << 27));
+    }
+  }
+}
+
+__device__ __forceinline__ void fq_emit(FillQ& Q, int lane, bool open, int q, uint32_t e_l,
+                                        unsigned sz_l, unsigned c0_l, unsigned mych) {
+  const unsigned nop = open ? mych : 0u;
+  unsigned incl;
+  const unsigned total = fq_scan(lane, nop, incl);
+  if (!total) return;
+  int base = lane == 0 ? atomicAdd(&Q.n, (int)total) : 0;
+  base = __shfl_sync(0xffffffffu, base, 0);
+  fq_write(Q, lane, (unsigned)base, total, incl, nop, q, e_l, sz_l, c0_l);
+}
+
+template <int G>
+__device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot, int s, FillQ& Q,
+                                              unsigned long long* sim = nullptr) {
+  const int N = a.g.N;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int P = a.ts.nparts, NB = gridDim.x;
+  const int nu = (P - (int)blockIdx.x + NB - 1) / NB;  // this CTA's units: blockIdx.x + k * NB
+  const size_t off = (size_t)slot * N;
+  const uint32_t* pre = a.ts.pre + off;
+  const uint16_t* szp = a.ts.szp + off;
+  const float* tdp = a.ts.tdp + off;
+  const unsigned T = __ldg(&a.ts.T[slot]);
+  const unsigned tq = T / (unsigned)P, tr = T % (unsigned)P;
+  const unsigned long long t_a0 = sim ? gtimer() : 0ull;
+  const MarkLayout L = a.L;
+  unsigned lnew = 0;
+  // ---- phase A ----
+  const uint32_t* part = a.ts.part + (size_t)slot * P;
+  for (int k0 = wid; k0 < nu; k0 += 4 * nw) {
+    uint32_t hpw = 0;
+    unsigned hcnt = 0;
+    if (lane < 4) {
+      const int k = k0 + lane * nw;
+      if (k < nu) {
+        const unsigned p = blockIdx.x + (unsigned)k * NB;
+        hpw = __ldg(&part[p]);  // in flight with T
+        // floor((p+1)T/P) - floor(pT/P) with T = tq*P + tr, in 32-bit arithmetic
+        hcnt = P < 65536 ? tq + ((p + 1) * tr) / (unsigned)P - (p * tr) / (unsigned)P
+                         : (unsigned)((((unsigned long long)p + 1) * T) / P - ((unsigned long long)p * T) / P);
+        if (!hcnt) hpw = 0;
+      }
+    }
+    const bool stamp = sim && blockIdx.x == 0 && threadIdx.x == 0 && k0 == wid;
+    unsigned q4[4], co4[4], sz4[4];
+    uint32_t e4[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const uint32_t pw = __shfl_sync(0xffffffffu, hpw, i);
+      q4[i] = pw & 0xFFFFu;
+      co4[i] = pw >> 16;
+      const int qa = (int)q4[i] + lane;
+      sz4[i] = 0;
+      e4[i] = 0;
+      if (qa < N) {
+        sz4[i] = __ldg(&szp[qa]);
+        e4[i] = __ldg(&pre[qa]);
+      }
+    }
+    unsigned cn4[4], tot = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      cn4[i] = __shfl_sync(0xffffffffu, hcnt, i);
+      tot += cn4[i];
+    }
+    int ok = 0;  // room for all four units (upper bound: every chunk open)
+    if (lane == 0 && tot) {
+      const int r = atomicAdd(&Q.res, (int)tot);
+      ok = r + (int)tot <= FQ_CAP;
+      if (!ok) atomicSub(&Q.res, (int)tot);
+    }
+    if (!tot) continue;
+    if (!__shfl_sync(0xffffffffu, ok, 0)) {  // deep tree: fill these units in place
+      for (int i = 0; i < 4; i++)
+        if (cn4[i]) lnew += fill_unit<(G > 4 ? 4 : G)>(a, slot, s, (int)blockIdx.x + (k0 + i * nw) * NB);
+      continue;
+    }
+    if (stamp) sim[4] = gtimer() - t_a0 + (unsigned long long)(q4[0] + q4[1] + q4[2] + q4[3]) * 0ull;
+    unsigned my4[4], c04[4], tk4[4];
+    int cv4[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      tk4[i] = fq_window(lane, (int)q4[i] + lane, sz4[i], co4[i], cn4[i], my4[i], c04[i]);
+      const int u_l = (int)(e4[i] & 0xFFFFu);
+      cv4[i] = (my4[i] && u_l != s) ? __ldcg(&a.cnt[u_l]) : 0;
+    }
+    if (stamp) sim[5] = gtimer() - t_a0 + (unsigned long long)(tk4[0] + tk4[3]) * 0ull;
+    // first windows of the four units: one reservation, independent chains
+    unsigned nop4[4], inc4[4], wt4[4], wsum = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      nop4[i] = (my4[i] && cv4[i] < N - 1) ? my4[i] : 0u;
+      wt4[i] = fq_scan(lane, nop4[i], inc4[i]);
+      wsum += wt4[i];
+    }
+    int base = lane == 0 && wsum ? atomicAdd(&Q.n, (int)wsum) : 0;
+    base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      fq_write(Q, lane, (unsigned)base, wt4[i], inc4[i], nop4[i], (int)q4[i], e4[i], sz4[i], c04[i]);
+      base += (int)wt4[i];
+    }
+    if (stamp) sim[6] = gtimer() - t_a0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      unsigned count = cn4[i] - tk4[i];
+      int q = (int)q4[i];
+      while (count) {  // further windows of a long unit
+        q += 32;
+        const int qa = q + lane;
+        unsigned sz_l = 0, mych, c0_l;
+        uint32_t e_l = 0;
+        if (qa < N) {
+          sz_l = __ldg(&szp[qa]);
+          e_l = __ldg(&pre[qa]);
+        }
+        const unsigned take = fq_window(lane, qa, sz_l, 0u, count, mych, c0_l);
+        const int u_l = (int)(e_l & 0xFFFFu);
+        const bool full_l = mych && u_l != s && __ldcg(&a.cnt[u_l]) >= N - 1;
+        fq_emit(Q, lane, mych && !full_l, q, e_l, sz_l, c0_l, mych);
+        count -= take;
+      }
+    }
+  }
+  if (sim && blockIdx.x == 0 && threadIdx.x == 0) sim[7] = gtimer() - t_a0;
+  __syncthreads();
+  if (sim && threadIdx.x == 0) {  // debug: CTA phase-A time (sum, max)
+    const unsigned long long dt = gtimer() - t_a0;
+    atomicAdd(&sim[2], dt);
+    atomicMax(&sim[3], dt);
+  }
+  // ---- phase B ----
+  // Only the pre entry and the mark word of each descriptor stay live across
+  // the loads; the descriptor is re-read from shared memory for new pairs.
+  const int nq = *(volatile int*)&Q.n;
+  int i0 = lane == 0 ? atomicAdd(&Q.head, G) : 0;
+  i0 = __shfl_sync(0xffffffffu, i0, 0);
+  while (i0 < nq) {
+    const int inext = lane == 0 ? atomicAdd(&Q.head, G) : 0;
+    uint32_t ew[G], word[G];
+#pragma unroll
+    for (int j = 0; j < G; j++) {
+      const uint2 d = i0 + j < nq ? Q.desc[i0 + j] : make_uint2(0u, 0u);
+      const bool v = i0 + j < nq && (unsigned)lane <= (d.y >> 27);
+      const unsigned qb = d.y & 0xFFFFu, c = (d.y >> 16) & 0x7FFu;
+      ew[j] = v ? __ldg(&pre[qb + c * 32u + lane]) : 0u;
+      word[j] = v ? 0u : 0xFFFFFFFFu;
+    }
+    unsigned need = 0;  // bit j: lane still has to read the mark word of descriptor j
+#pragma unroll
+    for (int j = 0; j < G; j++) need |= word[j] ? 0u : (1u << j);
+#pragma unroll
+    for (int j = 0; j < G; j++) {
+      if ((need >> j) & 1u) {
+        const int u = (int)(Q.desc[i0 + j].x & 0xFFFFu);
+        word[j] = ld_mark(a.mark + (size_t)u * L.RW + (ew[j] >> 21));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < G; j++) {
+      const uint32_t wcol = ew[j] >> 16;
+      const bool isnew = !((word[j] >> (wcol & 31)) & 1u);
+      const unsigned m = __ballot_sync(0xffffffffu, isnew);
+      if (m) {
+        const uint2 d = Q.desc[i0 + j];
+        const int u = (int)(d.x & 0xFFFFu);
+        if (isnew) {
+          const int w = (int)(ew[j] & 0xFFFFu);
+          const uint32_t ucol = d.x >> 16;
+          const unsigned qb = d.y & 0xFFFFu, c = (d.y >> 16) & 0x7FFu;
+          set_mark(a, u, wcol);
+          set_mark(a, w, ucol);
+          const float duv = __fsub_rn(__ldg(&tdp[qb + c * 32u + lane]), __ldg(&tdp[qb - 1]));
+          a.D[(size_t)u * N + w] = duv;
+          a.D[(size_t)w * N + u] = duv;
+          atomicAdd(&a.cnt[w], 1);
+        }
+        if (lane == 0) {
+          if (u != s) atomicAdd(&a.cnt[u], __popc(m));
+          lnew += __popc(m);
+        }
+      }
+    }
+    i0 = __shfl_sync(0xffffffffu, inext, 0);
+  }
+  return lnew;
 }
 
 // K2 for the root: (s, x) is an ancestor pair for every x, so the fill of
@@ -209,7 +510,7 @@ __device__ __forceinline__ unsigned fill_root_row(const CommitArgs& a, int slot,
   const int N = a.g.N;
   const MarkLayout L = a.L;
   const size_t off = (size_t)slot * N;
-  const uint16_t* tin = a.ts.tin + off;
+  const uint32_t* tin = a.ts.tin + off;
   const float* tdp = a.ts.tdp + off;
   uint32_t* row = a.mark + (size_t)s * L.RW;
   const uint32_t scol = mcol(L, (uint32_t)s);
@@ -231,8 +532,8 @@ __device__ __forceinline__ unsigned fill_root_row(const CommitArgs& a, int slot,
       // the lanes sharing a mark word OR their bits; their leader stores once
       const uint32_t acc = __reduce_or_sync(peers, 1u << (xcol & 31));
       if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(&row[xcol >> 5], acc);
-      atomicOr(&a.mark[mword(L, (uint32_t)x, scol)], sbit);
-      const float d = __ldg(&tdp[__ldg(&tin[x])]);
+      set_mark(a, x, scol);
+      const float d = __ldg(&tdp[__ldg(&tin[x]) & 0xFFFFu]);
       a.D[(size_t)s * N + x] = d;
       a.D[(size_t)x * N + s] = d;
       atomicAdd(&a.cnt[x], 1);
@@ -275,38 +576,56 @@ __device__ __forceinline__ void grid_barrier(GridBarrier* bar, unsigned& gen) {
 
 // K2, late phase: test every remaining unfilled pair (u, w) against the
 // committed tree's Euler intervals: u is an ancestor of w iff
-// tin[u] < tin[w] <= tin[u] + szp[tin[u]].  Work per commit = unfilled pairs
-// (shrinking), instead of the tree's ~N*depth pairs.
+// tin[u] < tin[w] <= tin[u] + sz[u] (tin and sz packed per pixel, so both
+// ends of a pair cost one gather each).  Work per commit = unfilled pairs
+// (shrinking), instead of the tree's ~N*depth pairs; LU entries per thread
+// are in flight together.
+constexpr int LU = 4;
 __device__ __forceinline__ unsigned fill_list(const CommitArgs& a, int slot, int s,
                                               unsigned cur, unsigned n) {
   const int N = a.g.N;
   const size_t off = (size_t)slot * N;
-  const uint16_t* tin = a.ts.tin + off;
-  const uint16_t* szp = a.ts.szp + off;
+  const uint32_t* tinz = a.ts.tin + off;
   const float* tdp = a.ts.tdp + off;
   const MarkLayout L = a.L;
   uint32_t* list = a.plist[cur];
   unsigned mine = 0;
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t e = __ldcg(&list[i]);
-    if (e == LIST_DEAD) continue;
-    const int u = (int)(e >> 16), w = (int)(e & 0xFFFFu);
-    const unsigned tu = __ldg(&tin[u]), tw = __ldg(&tin[w]);
-    int anc = -1, des = -1;
-    unsigned ta = 0, td = 0;
-    if (tu < tw && tw <= tu + __ldg(&szp[tu])) { anc = u; des = w; ta = tu; td = tw; }
-    else if (tw < tu && tu <= tw + __ldg(&szp[tw])) { anc = w; des = u; ta = tw; td = tu; }
-    if (anc < 0) continue;
-    const uint32_t ca = mcol(L, (uint32_t)anc), cd = mcol(L, (uint32_t)des);
-    atomicOr(&a.mark[mword(L, (uint32_t)anc, cd)], 1u << (cd & 31));
-    atomicOr(&a.mark[mword(L, (uint32_t)des, ca)], 1u << (ca & 31));
-    const float duv = __fsub_rn(__ldg(&tdp[td]), __ldg(&tdp[ta]));
-    a.D[(size_t)anc * N + des] = duv;
-    a.D[(size_t)des * N + anc] = duv;
-    if (anc != s) atomicAdd(&a.cnt[anc], 1);
-    atomicAdd(&a.cnt[des], 1);
-    list[i] = LIST_DEAD;
-    mine++;
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += LU * stride) {
+    uint32_t e[LU], zu[LU], zw[LU];
+#pragma unroll
+    for (int j = 0; j < LU; j++) {
+      const unsigned i = i0 + j * stride;
+      e[j] = i < n ? __ldcg(&list[i]) : LIST_DEAD;
+    }
+#pragma unroll
+    for (int j = 0; j < LU; j++) {
+      zu[j] = zw[j] = 0u;
+      if (e[j] != LIST_DEAD) {
+        zu[j] = __ldg(&tinz[e[j] >> 16]);
+        zw[j] = __ldg(&tinz[e[j] & 0xFFFFu]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < LU; j++) {
+      if (e[j] == LIST_DEAD) continue;
+      const unsigned tu = zu[j] & 0xFFFFu, tw = zw[j] & 0xFFFFu;
+      int anc, des;
+      unsigned ta, td;
+      if (tu < tw && tw <= tu + (zu[j] >> 16)) { anc = (int)(e[j] >> 16); des = (int)(e[j] & 0xFFFFu); ta = tu; td = tw; }
+      else if (tw < tu && tu <= tw + (zw[j] >> 16)) { anc = (int)(e[j] & 0xFFFFu); des = (int)(e[j] >> 16); ta = tw; td = tu; }
+      else continue;
+      const uint32_t ca = mcol(L, (uint32_t)anc), cd = mcol(L, (uint32_t)des);
+      atomicOr(&a.mark[mword(L, (uint32_t)anc, cd)], 1u << (cd & 31));
+      atomicOr(&a.mark[mword(L, (uint32_t)des, ca)], 1u << (ca & 31));
+      const float duv = __fsub_rn(__ldg(&tdp[td]), __ldg(&tdp[ta]));
+      a.D[(size_t)anc * N + des] = duv;
+      a.D[(size_t)des * N + anc] = duv;
+      if (anc != s) atomicAdd(&a.cnt[anc], 1);
+      atomicAdd(&a.cnt[des], 1);
+      list[i0 + j * stride] = LIST_DEAD;
+      mine++;
+    }
   }
   return mine;
 }
@@ -335,7 +654,11 @@ template <int G, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   __shared__ unsigned long long red64[32];
   __shared__ int unit_ctr[2];  // per-CTA work-unit counters (alternating steps)
-  if (threadIdx.x == 0) unit_ctr[0] = unit_ctr[1] = 0;
+  __shared__ FillQ fq;         // per-CTA chunk queue (tree mode)
+  if (threadIdx.x == 0) {
+    unit_ctr[0] = unit_ctr[1] = 0;
+    fq.n = fq.res = fq.head = 0;
+  }
   __syncthreads();
   const int N = a.g.N;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -380,6 +703,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     unsigned long long lnew = 0;
     if (mode == 1) {
       lnew = fill_list(a, slot, s, lcur, ln);
+    } else if (a.fillq) {
+      lnew = fill_tree_cta<G>(a, slot, s, fq, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr);
     } else {
       // Work units of this tree are interleaved over the CTAs (unit = b + k *
       // nblocks) and pulled by the CTA's warps from a shared counter, so the
@@ -389,7 +714,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
       const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
       if (PU <= nwarps) {  // one unit per warp: static
         const int u = (int)blockIdx.x * (int)(blockDim.x >> 5) + (int)(threadIdx.x >> 5);
-        if (u < PU) lnew = fill_unit<G>(a, slot, s, u);
+        if (u < PU) lnew = fill_unit<(G > 4 ? 4 : G)>(a, slot, s, u, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr);
       } else {
         int* ctr = &unit_ctr[step & 1];
         int k = lane == 0 ? atomicAdd(ctr, 1) : 0;
@@ -398,7 +723,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
           const int u = (int)blockIdx.x + k * (int)gridDim.x;
           if (u >= PU) break;
           int nk = lane == 0 ? atomicAdd(ctr, 1) : 0;
-          lnew += fill_unit<G>(a, slot, s, u);
+          unsigned* ust = (a.dbgu && step == a.dbgu_step) ? a.dbgu + (size_t)u * 8 : nullptr;
+          const unsigned long long tu0 = ust ? gtimer() : 0ull;
+          lnew += fill_unit<(G > 4 ? 4 : G)>(a, slot, s, u, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr, ust);
+          if (ust && lane == 0) {
+            ust[0] = (unsigned)(gtimer() - tu0);
+            ust[5] = blockIdx.x;
+            ust[6] = threadIdx.x >> 5;
+            ust[7] = (unsigned)(tu0 - tw0);
+          }
           k = __shfl_sync(0xffffffffu, nk, 0);
         }
         if (threadIdx.x == 0) unit_ctr[(step & 1) ^ 1] = 0;  // next step's counter
@@ -408,10 +741,16 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     if (dbg) dbg[1] = gtimer();
     if (a.dbgw && (threadIdx.x & 31) == 0) {
       const unsigned long long dt = gtimer() - tw0;
-      atomicMax(&a.dbgw[(size_t)step * 2], dt);
-      atomicAdd(&a.dbgw[(size_t)step * 2 + 1], dt);
+      atomicMax(&a.dbgw[(size_t)step * 4], dt);
+      atomicAdd(&a.dbgw[(size_t)step * 4 + 1], dt);
     }
     lnew = block_reduce_sum(lnew, red64);
+    if (threadIdx.x == 0) fq.n = fq.res = fq.head = 0;  // all warps are past the fill
+    if (a.dbgw && threadIdx.x == 0) {
+      const unsigned long long dt = gtimer() - tw0;
+      atomicMax(&a.dbgw[(size_t)step * 4 + 2], dt);
+      atomicAdd(&a.dbgw[(size_t)step * 4 + 3], dt);
+    }
     if (threadIdx.x == 0 && lnew) atomicAdd(&a.newp[step], lnew);
     grid_barrier(a.bar, gen);
     if (dbg) dbg[2] = gtimer();
@@ -463,7 +802,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   }
 }
 
-// Fill pipelining depth G (chunks in flight per warp) = 4 fits 64 registers.
+// Fill pipelining depth G (chunk descriptors in flight per warp, default 4).
 // CTA shape: GP_COMMIT_THREADS = 512 (2 CTAs/SM, default) or 1024 (1 CTA/SM).
 int commit_threads() {
   static int t = 0;
@@ -474,17 +813,18 @@ int commit_threads() {
   return t;
 }
 
-// G = fill loop unroll (pairs in flight per lane per ancestor): GP_FILL_UNROLL
+// G = chunks in flight per warp (GP_FILL_UNROLL = 1, 2, 4, 8)
 static const void* commit_kernel(int G) {
-  return G >= 4 ? (const void*)k_commit<4, 512, 2>
+  return G >= 8 ? (const void*)k_commit<8, 512, 2>
+       : G >= 4 ? (const void*)k_commit<4, 512, 2>
        : G == 1 ? (const void*)k_commit<1, 512, 2> : (const void*)k_commit<2, 512, 2>;
 }
 
 int commit_fill_depth() {
   static int g = 0;
   if (!g) {
-    g = 2;
-    if (const char* e = getenv("GP_FILL_UNROLL")) g = atoi(e) >= 4 ? 4 : atoi(e) == 1 ? 1 : 2;
+    g = 4;
+    if (const char* e = getenv("GP_FILL_UNROLL")) g = atoi(e) >= 8 ? 8 : atoi(e) >= 4 ? 4 : atoi(e) == 1 ? 1 : 2;
   }
   return g;
 }

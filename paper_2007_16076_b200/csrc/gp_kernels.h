@@ -25,7 +25,7 @@ struct TreeStore {
   uint32_t* part;
   uint32_t* T;
   uint32_t* C;  // ancestor/descendant pairs of the tree = sum of depths
-  uint16_t* tin;  // preorder position of each pixel (list-mode ancestor tests)
+  uint32_t* tin;  // per pixel: preorder position | descendant count << 16 (Euler interval)
   int nparts;  // commit warps (partition count)
   int cap;     // slots
 };
@@ -103,7 +103,11 @@ struct CommitArgs {
   Ctl* ctl;
   int max_steps;           // commits allowed in this launch
   unsigned long long* dbg; // optional per-step stamps [steps][4] from block 0 (debug)
-  unsigned long long* dbgw; // optional per-step warp fill times [steps][2] = (max, sum) ns
+  unsigned long long* dbgw; // optional per-step fill times [steps][4] = warp (max, sum), CTA (max, sum) ns
+  unsigned long long* dbgs; // optional per-step fill cost model [steps][4] (GP_DEBUG_SIM)
+  int fillq;                // tree-mode fill through the per-CTA chunk queue (default 1)
+  unsigned* dbgu;           // optional per-unit stats of step dbgu_step (GP_DEBUG_UNITS)
+  int dbgu_step;
   GridBarrier* bar;
   uint32_t* plist[2];      // unfilled pairs (u << 16 | w, u < w), list mode
   unsigned long long total_pairs;

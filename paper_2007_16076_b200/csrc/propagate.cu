@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   const int lane = tid & 31, wid = tid >> 5;
   if (a.ntrees_dev && t >= *a.ntrees_dev) return;
   __shared__ PropShared sh;
-  unsigned long long* dbg = a.dbg ? a.dbg + (size_t)t * 8 : nullptr;
+  unsigned long long* dbg = a.dbg ? a.dbg + (size_t)t * 16 : nullptr;
   if (dbg && tid == 0) dbg[0] = gtimer();
 
   const size_t hist_cap = HIST_SMEM;
@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   atomicMax(&sh.maxd, lmax);
   __syncthreads();
   const int maxd = sh.maxd;
+  if (dbg && tid == 0) { dbg[8] = gtimer(); dbg[11] = maxd; }
   const bool use_hist = (size_t)maxd + 1 <= hist_cap;
   uint16_t* szv = reinterpret_cast<uint16_t*>(base + lay.A);  // descendants
   volatile uint16_t* vszv = szv;
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     }
   }
   __syncthreads();
+  if (dbg && tid == 0) dbg[9] = gtimer();
   // E4: descendant counts, deepest level first -- one warp, no block barriers
   // (shared-memory variant); block-wide per level in the global variant,
   // where one warp would pay a global round trip per level and element
@@ -495,6 +497,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     }
   }
   __syncthreads();
+  if (dbg && tid == 0) dbg[10] = gtimer();
   // sizes move to B (depth is dead) so that A can hold the path-sum words
   volatile uint16_t* szB = reinterpret_cast<volatile uint16_t*>(base + lay.B);
   for (int v = tid; v < N; v += nthr) szB[v] = vszv[v];
@@ -538,11 +541,11 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     return gm ? __ldcg(const_cast<const unsigned short*>(p)) : *p;
   };
   float* gtdp = a.ts.tdp + off;
-  uint16_t* gtin = a.ts.tin + off;
+  uint32_t* gtin = a.ts.tin + off;
   for (int v = tid; v < N; v += nthr) {
     const uint32_t q = rd32(&pj[v]) >> 16;
     gtdp[q] = __uint_as_float(rd32(&vdist[v]));
-    gtin[v] = (uint16_t)q;
+    gtin[v] = q | ((uint32_t)rd16(&szB[v]) << 16);
   }
   __syncthreads();
   volatile uint16_t* preS = reinterpret_cast<volatile uint16_t*>(base);
