@@ -709,6 +709,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     unsigned long long* d_cdbg = nullptr;
     unsigned long long* d_pdbg = nullptr;
     std::vector<double> pacc(16, 0.0);
+    double e6acc = 0.0;
     long long pn = 0;
     auto fold_pdbg = [&]() {  // per-tree phase stamps of the last (completed) batch
       if (!d_pdbg) return;
@@ -726,6 +727,10 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
         pacc[10] += (double)(r[10] - r[9]);
         pacc[11] += (double)(r[4] - r[10]);
         pacc[12] += (double)r[11];
+        pacc[13] += (double)r[12];
+        pacc[14] += (double)r[13];
+        pacc[15] += (double)(r[14] - r[10]);
+        e6acc += (double)(r[15] - r[4]);
         pn++;
       }
     };
@@ -862,8 +867,11 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
                 pacc[1] / 1e3 / pn, pacc[2] / 1e3 / pn, pacc[3] / 1e3 / pn, pacc[4] / 1e3 / pn,
                 pacc[5] / 1e3 / pn, pacc[6] / pn, pacc[7] / pn / N, pn);
       if (pn)
-        fprintf(stderr, "[gp debug] levels split (us): depth %.1f sort %.1f sizes %.1f preorder %.1f | mean maxdepth %.1f\n",
-                pacc[8] / 1e3 / pn, pacc[9] / 1e3 / pn, pacc[10] / 1e3 / pn, pacc[11] / 1e3 / pn, pacc[12] / pn);
+        fprintf(stderr, "[gp debug] levels split (us): depth %.1f sort %.1f sizes %.1f preorder %.1f | mean maxdepth %.1f | bucket advances %.1f taking %.1f us\n",
+                pacc[8] / 1e3 / pn, pacc[9] / 1e3 / pn, pacc[10] / 1e3 / pn, pacc[11] / 1e3 / pn, pacc[12] / pn,
+                pacc[14] / pn, pacc[13] / 1e3 / pn);
+      if (pn)
+        fprintf(stderr, "[gp debug] E5 offsets %.1f us, E6 arrays %.1f us\n", pacc[15] / 1e3 / pn, e6acc / 1e3 / pn);
       cudaFree(d_pdbg);
     }
     for (auto& e : cev) { S.ms_commit += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }

@@ -45,7 +45,6 @@ extern __shared__ __align__(16) unsigned char g_smem[];
 
 constexpr int HIST_SMEM = 4096;  // depth-histogram bins in the shared-memory variant
 constexpr int WL_SMEM = 12288;   // worklist entries kept in smem (global-scratch variant)
-constexpr int BIG_MAX = 64;      // queued many-unit preorder positions (partition writes)
 
 struct PropShared {
   int cnt[2];
@@ -56,7 +55,6 @@ struct PropShared {
   unsigned total;
   unsigned pairs;
   int nbig;
-  unsigned big[64][4];
 };
 
 struct Layout {
@@ -173,7 +171,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   if (a.ntrees_dev && t >= *a.ntrees_dev) return;
   __shared__ PropShared sh;
   unsigned long long* dbg = a.dbg ? a.dbg + (size_t)t * 16 : nullptr;
-  if (dbg && tid == 0) dbg[0] = gtimer();
+  if (dbg && tid == 0) { dbg[0] = gtimer(); dbg[12] = 0; dbg[13] = 0; }
 
   const size_t hist_cap = HIST_SMEM;
   const Layout lay = prop_layout(N, hist_cap);
@@ -236,6 +234,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   for (;;) {
     int n = sh.cnt[cur];
     if (n == 0) {
+      const unsigned long long ta0 = dbg ? gtimer() : 0ull;
       // bucket advance: min over the far pixels, then move those <= thr
       uint32_t lmin = INF_BITS;
       for (int w = tid; w < NW; w += nthr) {
@@ -290,6 +289,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
       }
       __syncthreads();
       n = sh.cnt[cur];
+      if (dbg && tid == 0) { dbg[12] += gtimer() - ta0; dbg[13]++; }
     }
     passes++;
     items_total += n;
@@ -300,6 +300,55 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     }
     if (tid == 0) sh.cnt[cur ^ 1] = 0;
     __syncthreads();
+    if (!a.in_smem) {
+      // global variant: RR rounds of (item, edge) pairs per thread in flight
+      // together -- distance loads, then independent atomics at L2
+      constexpr int RR = 4;
+      const int items = n * 8;
+      for (int b0 = 0; b0 < items; b0 += RR * nthr) {
+        int uk[RR];
+        uint32_t nbk[RR], oldk[RR], dvk[RR];
+        float fwk[RR];
+#pragma unroll
+        for (int j = 0; j < RR; j++) {
+          const int idx = b0 + j * nthr + tid;
+          uk[j] = -1;
+          dvk[j] = INF_BITS;
+          if (idx < items) {
+            const int v = *wl.at(cur, idx >> 3);
+            int k = idx & 7;
+            k += (k >= 4);
+            if (k_in_conn(g.conn, k)) {
+              const int r = v / g.W, c = v - r * g.W;
+              uk[j] = nbr_at(g, r, c, k);
+              if (uk[j] >= 0) {
+                dvk[j] = __ldcg(&dist[v]);
+                fwk[j] = edge_w(g.metric, __ldg(&f[v]), __ldg(&f[uk[j]]));
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < RR; j++) {
+          nbk[j] = uk[j] >= 0 ? __float_as_uint(__fadd_rn(__uint_as_float(dvk[j]), fwk[j])) : INF_BITS;
+          oldk[j] = uk[j] >= 0 ? atomicMin(&dist[uk[j]], nbk[j]) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < RR; j++) {
+          bool app = false;
+          const int u = uk[j];
+          if (u >= 0 && nbk[j] < oldk[j]) {
+            const uint32_t ub = 1u << (u & 31);
+            if (__uint_as_float(nbk[j]) <= thr) app = !(atomicOr(&inq[u >> 5], ub) & ub);
+            else atomicOr(&far[u >> 5], ub);
+          }
+          warp_append(app, u, &sh.cnt[cur ^ 1], wl, cur ^ 1);
+        }
+      }
+      cur ^= 1;
+      __syncthreads();
+      continue;
+    }
     const int items = n * 8;
     for (int b0 = 0; b0 < items; b0 += nthr) {
       const int idx = b0 + tid;
@@ -419,13 +468,31 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   if (a.in_smem) pointer_jump(pj, N);
   else pointer_jump_global(const_cast<uint32_t*>(pj), N);
   if (dbg && tid == 0) dbg[3] = gtimer();
+  // Loops over arrays that are stable within a phase read them from L2 in the
+  // global variant (__ldcg: no stale L1) and directly in shared memory; UB
+  // iterations' loads are issued before any is consumed.
+  const bool gm = !a.in_smem;
+  auto rd32 = [gm](const volatile uint32_t* p) -> uint32_t {
+    return gm ? __ldcg(const_cast<const uint32_t*>(p)) : *p;
+  };
+  auto rd16 = [gm](const volatile uint16_t* p) -> uint16_t {
+    return gm ? __ldcg(const_cast<const unsigned short*>(p)) : *p;
+  };
+  constexpr int UB = 8;
   // E2: depth (B) and max depth
   volatile uint16_t* depth = reinterpret_cast<volatile uint16_t*>(base + lay.B);
   int lmax = 0;
-  for (int v = tid; v < N; v += nthr) {
-    const int d = (int)(pj[v] >> 16);
-    depth[v] = (uint16_t)d;
-    lmax = max(lmax, d);
+  for (int v0 = tid; v0 < N; v0 += UB * nthr) {
+    uint32_t x[UB];
+#pragma unroll
+    for (int j = 0; j < UB; j++) x[j] = v0 + j * nthr < N ? rd32(&pj[v0 + j * nthr]) : 0u;
+#pragma unroll
+    for (int j = 0; j < UB; j++) {
+      if (v0 + j * nthr >= N) break;
+      const int d = (int)(x[j] >> 16);
+      depth[v0 + j * nthr] = (uint16_t)d;
+      lmax = max(lmax, d);
+    }
   }
   atomicMax(&sh.maxd, lmax);
   __syncthreads();
@@ -441,7 +508,14 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   if (use_hist) {
     for (int i = tid; i <= maxd; i += nthr) hist[i] = 0;
     __syncthreads();
-    for (int v = tid; v < N; v += nthr) atomicAdd(&hist[depth[v]], 1u);
+    for (int v0 = tid; v0 < N; v0 += UB * nthr) {
+      uint16_t x[UB];
+#pragma unroll
+      for (int j = 0; j < UB; j++) x[j] = v0 + j * nthr < N ? rd16(&depth[v0 + j * nthr]) : 0;
+#pragma unroll
+      for (int j = 0; j < UB; j++)
+        if (v0 + j * nthr < N) atomicAdd(&hist[x[j]], 1u);
+    }
     __syncthreads();
     if (wid == 0) {  // exclusive scan of hist[0..maxd] by one warp
       unsigned carry = 0;
@@ -459,9 +533,13 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
       }
     }
     __syncthreads();
-    for (int v = tid; v < N; v += nthr) {
-      const unsigned pos = atomicAdd(&hist[depth[v]], 1u);
-      order[pos] = (uint16_t)v;
+    for (int v0 = tid; v0 < N; v0 += UB * nthr) {
+      uint16_t x[UB];
+#pragma unroll
+      for (int j = 0; j < UB; j++) x[j] = v0 + j * nthr < N ? rd16(&depth[v0 + j * nthr]) : 0;
+#pragma unroll
+      for (int j = 0; j < UB; j++)
+        if (v0 + j * nthr < N) order[atomicAdd(&hist[x[j]], 1u)] = (uint16_t)(v0 + j * nthr);
     }
   }
   __syncthreads();
@@ -500,32 +578,49 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   if (dbg && tid == 0) dbg[10] = gtimer();
   // sizes move to B (depth is dead) so that A can hold the path-sum words
   volatile uint16_t* szB = reinterpret_cast<volatile uint16_t*>(base + lay.B);
-  for (int v = tid; v < N; v += nthr) szB[v] = vszv[v];
+  for (int v0 = tid; v0 < N; v0 += UB * nthr) {
+    uint16_t x[UB];
+#pragma unroll
+    for (int j = 0; j < UB; j++) x[j] = v0 + j * nthr < N ? rd16(&vszv[v0 + j * nthr]) : 0;
+#pragma unroll
+    for (int j = 0; j < UB; j++)
+      if (v0 + j * nthr < N) szB[v0 + j * nthr] = x[j];
+  }
   __syncthreads();
   // E5: preorder positions.  Children of p are ordered by id; child v's block
   // starts after p and its earlier siblings' blocks:
   //   tin[v] = sum over the path root..v (root excluded) of 1 + off(a),
   //   off(a) = sum of (size + 1) over the earlier siblings of a,
   // evaluated by pointer jumping on (acc << 16 | jump) words in A.
-  for (int v = tid; v < N; v += nthr) {
-    const uint8_t cv = vcode[v];
-    if (cv == GP_ROOT) {
-      pj[v] = (uint32_t)v;
-      continue;
-    }
-    const int pp = parent_of(v, cv, g.W);
+  // One thread per parent p walks its <= 8 neighbours in increasing id
+  // (= neighbour order) and assigns each child its sibling offset; every
+  // non-root pixel is written by its parent's thread, the root by itself.
+  for (int pp = tid; pp < N; pp += nthr) {
+    if (vcode[pp] == GP_ROOT) pj[pp] = (uint32_t)pp;
     const int pr = pp / g.W, pc = pp - pr * g.W;
-    unsigned offs = 0;
+    int ch[9];
+    unsigned szc[9];
+#pragma unroll
     for (int k = 0; k < 9; k++) {
+      ch[k] = -1;
       if (!k_in_conn(g.conn, k)) continue;
       const int q = nbr_at(g, pr, pc, k);
-      if (q < 0 || q >= v) continue;
+      if (q < 0) continue;
       const uint8_t cq = vcode[q];
-      if (cq != GP_ROOT && parent_of(q, cq, g.W) == pp) offs += (unsigned)szB[q] + 1u;
+      if (cq != GP_ROOT && parent_of(q, cq, g.W) == pp) ch[k] = q;
     }
-    pj[v] = ((1u + offs) << 16) | (uint32_t)pp;
+#pragma unroll
+    for (int k = 0; k < 9; k++) szc[k] = ch[k] >= 0 ? rd16(&szB[ch[k]]) : 0u;
+    unsigned offs = 0;
+#pragma unroll
+    for (int k = 0; k < 9; k++) {
+      if (ch[k] < 0) continue;
+      pj[ch[k]] = ((1u + offs) << 16) | (uint32_t)pp;
+      offs += szc[k] + 1u;
+    }
   }
   __syncthreads();
+  if (dbg && tid == 0) dbg[14] = gtimer();
   if (a.in_smem) pointer_jump(pj, N);
   else pointer_jump_global(const_cast<uint32_t*>(pj), N);
   if (dbg && tid == 0) dbg[4] = gtimer();
@@ -533,48 +628,88 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   // (now free) distance region for coalesced stores and the partition scan.
   // The arrays read here are stable after the barriers: the global variant
   // reads them from L2 (__ldcg: no stale L1, loads pipeline), smem directly.
-  const bool gm = !a.in_smem;
-  auto rd32 = [gm](const volatile uint32_t* p) -> uint32_t {
-    return gm ? __ldcg(const_cast<const uint32_t*>(p)) : *p;
-  };
-  auto rd16 = [gm](const volatile uint16_t* p) -> uint16_t {
-    return gm ? __ldcg(const_cast<const unsigned short*>(p)) : *p;
-  };
   float* gtdp = a.ts.tdp + off;
   uint32_t* gtin = a.ts.tin + off;
-  for (int v = tid; v < N; v += nthr) {
-    const uint32_t q = rd32(&pj[v]) >> 16;
-    gtdp[q] = __uint_as_float(rd32(&vdist[v]));
-    gtin[v] = q | ((uint32_t)rd16(&szB[v]) << 16);
+  constexpr int UE = 4;
+  for (int v0 = tid; v0 < N; v0 += UE * nthr) {
+    uint32_t x[UE], dv[UE];
+    uint16_t sz[UE];
+#pragma unroll
+    for (int j = 0; j < UE; j++) {
+      const int v = v0 + j * nthr;
+      x[j] = v < N ? rd32(&pj[v]) : 0u;
+      dv[j] = v < N ? rd32(&vdist[v]) : 0u;
+      sz[j] = v < N ? rd16(&szB[v]) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < UE; j++) {
+      const int v = v0 + j * nthr;
+      if (v >= N) break;
+      const uint32_t q = x[j] >> 16;
+      gtdp[q] = __uint_as_float(dv[j]);
+      gtin[v] = q | ((uint32_t)sz[j] << 16);
+    }
   }
   __syncthreads();
   volatile uint16_t* preS = reinterpret_cast<volatile uint16_t*>(base);
   volatile uint16_t* szS = preS + N;
-  for (int v = tid; v < N; v += nthr) {
-    const unsigned q = rd32(&pj[v]) >> 16;
-    const uint16_t sz = rd16(&szB[v]);
-    preS[q] = (uint16_t)v;
-    szS[q] = sz;
+  for (int v0 = tid; v0 < N; v0 += UE * nthr) {
+    uint32_t x[UE];
+    uint16_t sz[UE];
+#pragma unroll
+    for (int j = 0; j < UE; j++) {
+      const int v = v0 + j * nthr;
+      x[j] = v < N ? rd32(&pj[v]) : 0u;
+      sz[j] = v < N ? rd16(&szB[v]) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < UE; j++) {
+      const int v = v0 + j * nthr;
+      if (v >= N) break;
+      preS[x[j] >> 16] = (uint16_t)v;
+      szS[x[j] >> 16] = sz[j];
+    }
   }
   __syncthreads();
   uint32_t* gpre = a.ts.pre + off;
   uint16_t* gszp = a.ts.szp + off;
   const MarkLayout ML = a.L;
-  for (int q = tid; q < N; q += nthr) {
-    const uint32_t v = rd16(&preS[q]);
-    gpre[q] = (mcol(ML, v) << 16) | v;
-    gszp[q] = rd16(&szS[q]);
+  for (int q0 = tid; q0 < N; q0 += UB * nthr) {
+    uint16_t pv[UB], sz[UB];
+#pragma unroll
+    for (int j = 0; j < UB; j++) {
+      const int q = q0 + j * nthr;
+      pv[j] = q < N ? rd16(&preS[q]) : 0;
+      sz[j] = q < N ? rd16(&szS[q]) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < UB; j++) {
+      const int q = q0 + j * nthr;
+      if (q >= N) break;
+      gpre[q] = (mcol(ML, pv[j]) << 16) | pv[j];
+      gszp[q] = sz[j];
+    }
+  }
+  if (dbg) {
+    __syncthreads();
+    if (tid == 0) dbg[15] = gtimer();
   }
   // E7: chunk counts ceil(szp/32), exclusive scan over preorder, partition
   const int seg = (N + nthr - 1) / nthr;
   const int q0 = min(N, tid * seg), q1 = min(N, q0 + seg);
   unsigned lsum = 0, lpairs = 0;
+  constexpr int US = 16;
   // the root (q = 0) pairs with every pixel; the commit kernel fills its row
   // with a grid-wide row scan, so its chunks are left out of the partition
-  for (int q = q0; q < q1; q++) {
-    const unsigned sq = rd16(&szS[q]);
-    lsum += q ? (sq + 31u) >> 5 : 0u;
-    lpairs += sq;
+  for (int qb = q0; qb < q1; qb += US) {
+    uint16_t x[US];
+#pragma unroll
+    for (int j = 0; j < US; j++) x[j] = qb + j < q1 ? rd16(&szS[qb + j]) : 0;
+#pragma unroll
+    for (int j = 0; j < US; j++) {
+      lsum += (qb + j) ? ((unsigned)x[j] + 31u) >> 5 : 0u;
+      lpairs += x[j];
+    }
   }
   atomicAdd(&sh.pairs, lpairs);
   unsigned incl = lsum;
@@ -623,30 +758,45 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   };
   // positions owning many units (near the root) are queued and written by
   // whole warps; the rest by their thread
+  // queue of many-part positions: the B region (sizes by pixel, dead after E6)
+  uint4* big = reinterpret_cast<uint4*>(base + lay.B);
+  const int bigcap = (int)(((size_t)N * 2) / sizeof(uint4));
   if (tid == 0) sh.nbig = 0;
   __syncthreads();
-  for (int q = q0; q < q1; q++) {
-    const unsigned nch = q ? ((unsigned)rd16(&szS[q]) + 31u) >> 5 : 0u;
-    if (!nch) continue;
-    // partitions p whose first chunk floor(p*T/P) lies in [run, run+nch)
-    const unsigned long long plo = first_part(run), phi = min(first_part(run + nch), P);
-    if (phi - plo > 32) {
-      const int i = atomicAdd(&sh.nbig, 1);
-      if (i < BIG_MAX) {
-        sh.big[i][0] = (unsigned)q; sh.big[i][1] = run;
-        sh.big[i][2] = (unsigned)plo; sh.big[i][3] = (unsigned)phi;
-        run += nch;
-        continue;
+  // parts are handed out in order: pn = first part not yet placed; the parts
+  // starting in position q are those with pn*T < (run + nch)*P
+  unsigned long long pn = first_part(run);
+  for (int qb = q0; qb < q1; qb += US) {
+    uint16_t x[US];
+#pragma unroll
+    for (int j = 0; j < US; j++) x[j] = qb + j < q1 ? rd16(&szS[qb + j]) : 0;
+    for (int j = 0; j < US && qb + j < q1; j++) {
+      const int q = qb + j;
+      const unsigned nch = q ? ((unsigned)x[j] + 31u) >> 5 : 0u;
+      if (!nch) continue;
+      const unsigned long long end = (unsigned long long)(run + nch) * P;
+      if (pn < P && pn * T < end) {
+        if ((pn + 4) * T < end) {  // several parts (the trunk near the root): queued for warps
+          const unsigned long long phi = min(first_part(run + nch), P);
+          const int i = atomicAdd(&sh.nbig, 1);
+          if (i < bigcap) {
+            big[i] = make_uint4((unsigned)q, run, (unsigned)pn, (unsigned)phi);
+          } else {
+            for (unsigned long long pp = pn; pp < phi; pp++) write_part(pp, (unsigned)q, run);
+          }
+          pn = phi;
+        } else {
+          while (pn < P && pn * T < end) write_part(pn++, (unsigned)q, run);
+        }
       }
+      run += nch;
     }
-    for (unsigned long long pp = plo; pp < phi; pp++) write_part(pp, (unsigned)q, run);
-    run += nch;
   }
   __syncthreads();
-  const int nbig = min(sh.nbig, BIG_MAX);
+  const int nbig = min(sh.nbig, bigcap);
   for (int i = wid; i < nbig; i += nthr >> 5) {
-    for (unsigned pp = sh.big[i][2] + lane; pp < sh.big[i][3]; pp += 32)
-      write_part(pp, sh.big[i][0], sh.big[i][1]);
+    const uint4 e = gm ? __ldcg(&big[i]) : big[i];
+    for (unsigned pp = e.z + lane; pp < e.w; pp += 32) write_part(pp, e.x, e.y);
   }
   if (dbg) {
     __syncthreads();
