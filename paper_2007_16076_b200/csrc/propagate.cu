@@ -400,20 +400,32 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   volatile uint8_t* vcode = code;
   int unparented = 0;
   for (int v = tid; v < N; v += nthr) {
-    const uint32_t dvb = vdist[v];
+    const uint32_t dvb = a.in_smem ? vdist[v] : __ldcg(&dist[v]);
     uint8_t cv = GP_ROOT;
     if (!((vfar[v >> 5] >> (v & 31)) & 1u)) {
       const float dv = __uint_as_float(dvb);
       const int r = v / g.W, c = v - r * g.W;
-      uint32_t best = INF_BITS;
-      for (int k = 0; k < 9; k++) {
+      const float fv = f[v];
+      uint32_t dub[9];
+      float fu[9];
+#pragma unroll
+      for (int k = 0; k < 9; k++) {  // all neighbour loads in flight together
+        dub[k] = INF_BITS;
+        fu[k] = 0.0f;
         if (!k_in_conn(g.conn, k)) continue;
         const int u = nbr_at(g, r, c, k);
         if (u < 0) continue;
-        const uint32_t dub = vdist[u];
-        const float cand = __fadd_rn(__uint_as_float(dub), edge_w(g.metric, f[u], f[v]));
-        if (cand == dv && (dub < dvb || (dub == dvb && u < v)) && dub < best) {
-          best = dub;
+        dub[k] = a.in_smem ? vdist[u] : __ldcg(&dist[u]);
+        fu[k] = f[u];
+      }
+      uint32_t best = INF_BITS;
+#pragma unroll
+      for (int k = 0; k < 9; k++) {
+        if (dub[k] == INF_BITS) continue;
+        const int u = v + (k / 3 - 1) * g.W + (k % 3 - 1);
+        const float cand = __fadd_rn(__uint_as_float(dub[k]), edge_w(g.metric, fu[k], fv));
+        if (cand == dv && (dub[k] < dvb || (dub[k] == dvb && u < v)) && dub[k] < best) {
+          best = dub[k];
           cv = (uint8_t)k;
         }
       }
@@ -548,11 +560,18 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   // (shared-memory variant); block-wide per level in the global variant,
   // where one warp would pay a global round trip per level and element
   if (use_hist && !a.in_smem) {
+    // the first entry of the next level is loaded before this level's barrier
+    int vn = -1;
+    if (maxd >= 1 && vhist[maxd - 1] + tid < vhist[maxd]) vn = order[vhist[maxd - 1] + tid];
     for (int d = maxd; d >= 1; d--) {
       const unsigned lo = vhist[d - 1], hi = vhist[d];
-      for (unsigned i = lo + tid; i < hi; i += nthr) {
+      const int v0 = vn;
+      vn = -1;
+      if (d >= 2 && vhist[d - 2] + tid < vhist[d - 1]) vn = order[vhist[d - 2] + tid];
+      if (v0 >= 0) atomic_add_u16(szv, parent_of(v0, vcode[v0], g.W), (unsigned)__ldcg(&szv[v0]) + 1u);
+      for (unsigned i = lo + nthr + tid; i < hi; i += nthr) {
         const int v = order[i];
-        atomic_add_u16(szv, parent_of(v, vcode[v], g.W), (unsigned)vszv[v] + 1u);
+        atomic_add_u16(szv, parent_of(v, vcode[v], g.W), (unsigned)__ldcg(&szv[v]) + 1u);
       }
       __syncthreads();
     }
@@ -595,28 +614,42 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   // One thread per parent p walks its <= 8 neighbours in increasing id
   // (= neighbour order) and assigns each child its sibling offset; every
   // non-root pixel is written by its parent's thread, the root by itself.
-  for (int pp = tid; pp < N; pp += nthr) {
-    if (vcode[pp] == GP_ROOT) pj[pp] = (uint32_t)pp;
-    const int pr = pp / g.W, pc = pp - pr * g.W;
-    int ch[9];
-    unsigned szc[9];
+  // Two parents per iteration: their children's sizes are loaded together.
+  for (int p0 = tid; p0 < N; p0 += 2 * nthr) {
+    unsigned mask[2] = {0u, 0u};
+    unsigned szc[2][9];
 #pragma unroll
-    for (int k = 0; k < 9; k++) {
-      ch[k] = -1;
-      if (!k_in_conn(g.conn, k)) continue;
-      const int q = nbr_at(g, pr, pc, k);
-      if (q < 0) continue;
-      const uint8_t cq = vcode[q];
-      if (cq != GP_ROOT && parent_of(q, cq, g.W) == pp) ch[k] = q;
+    for (int b = 0; b < 2; b++) {
+      const int pp = p0 + b * nthr;
+      if (pp >= N) continue;
+      if (vcode[pp] == GP_ROOT) pj[pp] = (uint32_t)pp;
+      const int pr = pp / g.W, pc = pp - pr * g.W;
+      // q = pp + offset(k) is a child iff its code points back: code == 8 - k
+      const bool interior = pr > 0 && pr < g.H - 1 && pc > 0 && pc < g.W - 1;
+#pragma unroll
+      for (int k = 0; k < 9; k++) {
+        if (!k_in_conn(g.conn, k)) continue;
+        if (!interior && nbr_at(g, pr, pc, k) < 0) continue;
+        if (vcode[pp + (k / 3 - 1) * g.W + (k % 3 - 1)] == (uint8_t)(8 - k)) mask[b] |= 1u << k;
+      }
     }
 #pragma unroll
-    for (int k = 0; k < 9; k++) szc[k] = ch[k] >= 0 ? rd16(&szB[ch[k]]) : 0u;
-    unsigned offs = 0;
+    for (int b = 0; b < 2; b++) {
+      const int pp = p0 + b * nthr;
 #pragma unroll
-    for (int k = 0; k < 9; k++) {
-      if (ch[k] < 0) continue;
-      pj[ch[k]] = ((1u + offs) << 16) | (uint32_t)pp;
-      offs += szc[k] + 1u;
+      for (int k = 0; k < 9; k++)
+        szc[b][k] = ((mask[b] >> k) & 1u) ? rd16(&szB[pp + (k / 3 - 1) * g.W + (k % 3 - 1)]) : 0u;
+    }
+#pragma unroll
+    for (int b = 0; b < 2; b++) {
+      const int pp = p0 + b * nthr;
+      unsigned offs = 0;
+#pragma unroll
+      for (int k = 0; k < 9; k++) {
+        if (!((mask[b] >> k) & 1u)) continue;
+        pj[pp + (k / 3 - 1) * g.W + (k % 3 - 1)] = ((1u + offs) << 16) | (uint32_t)pp;
+        offs += szc[b][k] + 1u;
+      }
     }
   }
   __syncthreads();
