@@ -13,9 +13,9 @@ see DESIGN.md), value = N * A * K / max-over-ranks(device time of K steps).
   propagation batches).  The image is resident on the device; L2 is flushed
   (256 MiB write) between steps (D at config 2 is only 64 MiB).
 * e2e = the same metric through the C ABI with host buffers: per step
-  gp_ctx_load (validation + H2D of the image from pinned memory) + gp_run +
-  gp_store_read of D into pinned host memory (D2H 4*N^2 bytes); wall clock
-  around the synchronous calls.
+  gp_ctx_load (validation + H2D of the image from pinned memory) +
+  gp_run_to_host (the run, with D streamed into pinned host memory as its
+  rows complete: D2H 4*N^2 bytes); wall clock around the synchronous calls.
 * roofline: dominant kernel = the commit loop (k_commit).  Algorithmic bytes
   per image B_alg = 4N^2 + N^2/8 + C/4 + 10*N*P with C the
   ancestor/descendant pairs of the committed trees (measured on device),
@@ -290,8 +290,8 @@ def main():
         t0 = time.perf_counter()
         _lib.check(L.gp_ctx_load(ctx, dtype, ctypes.c_void_p(px_pinned.data_ptr())))
         s2 = _lib.RunStats()
-        _lib.check(L.gp_run(ctx, st, strat, 0, 0, _lib.ptr(seq), _lib.ptr(new), ctypes.byref(s2)))
-        _lib.check(L.gp_store_read(st, ctypes.c_void_p(Dh.data_ptr()), None))
+        _lib.check(L.gp_run_to_host(ctx, st, strat, 0, 0, _lib.ptr(seq), _lib.ptr(new),
+                                     ctypes.byref(s2), ctypes.c_void_p(Dh.data_ptr())))
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = statistics.mean(e2e_times)

@@ -25,6 +25,7 @@
  *   gp_store_counts      DistanceArray.point_filled_counts distances.py:71-76
  *   gp_store_read        DistanceArray.dist / .mark        distances.py:55-58
  *   gp_run               run_strategy (naive, filling-rate) strategies.py:246-273
+ *   gp_run_to_host       run_strategy + DistanceArray.dist on the host, streamed
  *                        incl. _extrema_context            strategies.py:109-116
  *   gp_extrema           compute_extrema_context           strategies.py:104-116
  */
@@ -120,6 +121,14 @@ int gp_store_read(gp_store *st, float *D_out, uint8_t *mark_out);
  * spec_k: speculative batch size (0 = default). */
 int gp_run(gp_ctx *ctx, gp_store *st, int strategy, int naive_with_tree, int spec_k,
            int32_t *seq_out, int64_t *new_out, gp_run_stats *stats);
+
+/* gp_run + the host copy of D (fp32 [n][n], D_out; pinned memory lets the
+ * copy overlap the run): rows are streamed to the host as they complete
+ * (count n-1), the rest after the last commit.  Replaces run_strategy
+ * followed by reading DistanceArray.dist (strategies.py:246-273,
+ * distances.py:55) in one call. */
+int gp_run_to_host(gp_ctx *ctx, gp_store *st, int strategy, int naive_with_tree, int spec_k,
+                   int32_t *seq_out, int64_t *new_out, gp_run_stats *stats, float *D_out);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ EXPORTS = (
     "gp_ctx_num_pixels",
     "gp_propagate", "gp_propagate_batch", "gp_extrema", "gp_store_create", "gp_store_destroy",
     "gp_store_device_ptrs", "gp_store_fill_tree", "gp_store_fill_source", "gp_store_counts",
-    "gp_store_read", "gp_run",
+    "gp_store_read", "gp_run", "gp_run_to_host",
 )
 
 
@@ -78,6 +78,7 @@ def load_library(path: str = LIB_PATH, *, require_device: bool = True):
     L.gp_store_counts.argtypes = [P, P, P]
     L.gp_store_read.argtypes = [P, P, P]
     L.gp_run.argtypes = [P, P, i32, i32, i32, P, P, ctypes.POINTER(RunStats)]
+    L.gp_run_to_host.argtypes = [P, P, i32, i32, i32, P, P, ctypes.POINTER(RunStats), P]
     _lib = L
     if require_device:
         _require_device()

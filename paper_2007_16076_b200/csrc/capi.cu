@@ -40,6 +40,8 @@ struct gp_ctx {
   float* d_img = nullptr;
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;  // propagation stream (overlapped with the commit loop)
+  cudaStream_t st3 = nullptr;  // device-to-host stream of completed D rows (gp_run_to_host)
+  int* h_cnt = nullptr;        // pinned copy of the per-pixel counts
   int nsm = 148;
   // tree store (Euler-tour form) + propagation scratch, lazily sized
   TreeStore ts{};
@@ -172,6 +174,8 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
   cudaFree(c->scratch);
   if (c->st) cudaStreamDestroy(c->st);
   if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->st3) cudaStreamDestroy(c->st3);
+  if (c->h_cnt) cudaFreeHost(c->h_cnt);
   delete c;
 }
 
@@ -527,10 +531,62 @@ static int commit_blocks(gp_ctx* c, bool overlap) {
   return std::max(1, std::min(maxb, bps * c->nsm));
 }
 
+// Streamed result rows (gp_run_to_host): a row u of D is final once its count
+// reaches N-1 (every pair (u, *) is filled; the diagonal is set at reset).
+// Between commit launches the host reads the counts and queues the newly
+// complete rows (merged into contiguous runs) on a copy stream, so the D2H
+// transfer overlaps the rest of the run; the remaining rows follow at the end.
+struct RowStreamer {
+  gp_ctx* c;
+  gp_store* s;
+  float* host;
+  std::vector<uint8_t> sent;
+  int64_t rows_sent = 0;
+  int enqueue(bool all) {
+    const int N = c->g.N;
+    if (!host) return GP_OK;
+    if (!all) {
+      CUDA_TRY(cudaMemcpyAsync(c->h_cnt, s->cnt, (size_t)N * 4, cudaMemcpyDeviceToHost, c->st));
+      CUDA_TRY(cudaStreamSynchronize(c->st));
+    }
+    int u = 0;
+    while (u < N) {
+      if (sent[u] || (!all && c->h_cnt[u] != N - 1)) { u++; continue; }
+      int e = u;
+      while (e < N && !sent[e] && (all || c->h_cnt[e] == N - 1)) sent[e++] = 1;
+      CUDA_TRY(cudaMemcpyAsync(host + (size_t)u * N, s->D + (size_t)u * N, (size_t)(e - u) * N * 4,
+                               cudaMemcpyDeviceToHost, c->st3));
+      rows_sent += e - u;
+      u = e;
+    }
+    return GP_OK;
+  }
+};
+
+static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, int spec_k,
+                    int32_t* seq_out, int64_t* new_out, gp_run_stats* stats, float* D_host);
+
 extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, int spec_k,
                       int32_t* seq_out, int64_t* new_out, gp_run_stats* stats) {
+  return run_impl(c, s, strategy, naive_with_tree, spec_k, seq_out, new_out, stats, nullptr);
+}
+
+extern "C" int gp_run_to_host(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, int spec_k,
+                              int32_t* seq_out, int64_t* new_out, gp_run_stats* stats, float* D_out) {
+  if (!D_out) return fail(GP_EINVAL, "null D_out");
+  return run_impl(c, s, strategy, naive_with_tree, spec_k, seq_out, new_out, stats, D_out);
+}
+
+static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, int spec_k,
+                    int32_t* seq_out, int64_t* new_out, gp_run_stats* stats, float* D_host) {
   if (!c || !s) return fail(GP_EINVAL, "null argument");
   const int N = c->g.N;
+  RowStreamer rs{c, s, D_host, {}, 0};
+  if (D_host) {
+    rs.sent.assign(N, 0);
+    if (!c->st3) CUDA_TRY(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
+    if (!c->h_cnt) CUDA_TRY(cudaHostAlloc(&c->h_cnt, (size_t)N * 4, cudaHostAllocDefault));
+  }
   if (s->n != N) return fail(GP_EINVAL, "store size does not match the image");
   if (strategy != GP_STRATEGY_NAIVE && strategy != GP_STRATEGY_FILLING_RATE)
     return fail(GP_EINVAL, "strategy not supported on the device path");
@@ -819,6 +875,7 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
       CUDA_TRY(cudaStreamSynchronize(st));
       if (sl < 0) {
         if (int r = batch(0)) return r;
+        if (int r = rs.enqueue(false)) return r;  // overlaps the propagation batch
         CUDA_TRY(cudaStreamSynchronize(ps));
         fold_pdbg();
       }
@@ -881,6 +938,11 @@ extern "C" int gp_run(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree,
     P = h_ctl.step;
     S.propagations += h_ctl.total_props;
     S.visits = (int64_t)h_ctl.visits;
+  }
+  if (D_host && !rc) {
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (int r = rs.enqueue(true)) return r;
+    CUDA_TRY(cudaStreamSynchronize(c->st3));
   }
   S.ms_total = ev_ms(tot);
   S.ms_setup = ev_ms(setup);

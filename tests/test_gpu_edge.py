@@ -106,3 +106,38 @@ def test_metric_properties_of_completed_array(gp):
     rng = np.random.default_rng(9)
     x, y, z = (rng.integers(0, D.shape[0], 10_000) for _ in range(3))
     assert int((D[x, z] > D[x, y] + D[y, z]).sum()) == 0
+
+
+@pytest.mark.parametrize("shape,kind", [((40, 37), 1), ((64, 64), 1), ((23, 30), 0)])
+def test_run_to_host_streams_the_same_array(gp, shape, kind):
+    """gp_run_to_host (rows streamed during the run) == gp_run + gp_store_read."""
+    import ctypes
+
+    import torch
+
+    from paper_2007_16076_b200 import _lib
+
+    L = _lib.lib()
+    img = np.random.default_rng(shape[0] * 7 + kind).integers(1, 256, shape).astype(np.int64)
+    n = img.size
+    ctx = ctypes.c_void_p()
+    st = ctypes.c_void_p()
+    _lib.check(L.gp_ctx_create(shape[0], shape[1], 0, _lib.ptr(img), 1, 8, ctypes.byref(ctx)))
+    _lib.check(L.gp_store_create(n, ctypes.byref(st)))
+    try:
+        seq = np.zeros(n, np.int32)
+        new = np.zeros(n, np.int64)
+        stats = _lib.RunStats()
+        _lib.check(L.gp_run(ctx, st, kind, 0, 0, _lib.ptr(seq), _lib.ptr(new), ctypes.byref(stats)))
+        ref = np.empty((n, n), np.float32)
+        _lib.check(L.gp_store_read(st, _lib.ptr(ref), None))
+        for pinned in (True, False):
+            host = torch.full((n, n), -7.0, dtype=torch.float32, pin_memory=pinned)
+            seq2 = np.zeros(n, np.int32)
+            _lib.check(L.gp_run_to_host(ctx, st, kind, 0, 0, _lib.ptr(seq2), None, ctypes.byref(stats),
+                                        ctypes.c_void_p(host.data_ptr())))
+            assert np.array_equal(seq2, seq)
+            assert np.array_equal(host.numpy(), ref)
+    finally:
+        L.gp_store_destroy(st)
+        L.gp_ctx_destroy(ctx)
