@@ -182,7 +182,7 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
 extern "C" int gp_ctx_num_pixels(const gp_ctx* c) { return c ? c->g.N : 0; }
 
 enum { WS_SEQ, WS_NEW, WS_SRC, WS_SLOT_OF, WS_RANK, WS_EXT, WS_SELKEY, WS_FLAGS, WS_CTL, WS_DFC,
-       WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB };
+       WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK };
 
 template <typename T>
 static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
@@ -727,6 +727,8 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     if (const char* e = getenv("GP_LOOKAHEAD")) Q = atoi(e);
     CUDA_TRY(ws_get(c, WS_CANDS, &d_cands, K));
     CUDA_TRY(ws_get(c, WS_SLOTS, &d_slots, K));
+    unsigned* d_tkeys = nullptr;
+    CUDA_TRY(ws_get(c, WS_TOPK, &d_tkeys, (size_t)2 * N));
     int rcs = ensure_scratch(c, (size_t)K);
     if (rcs) return rcs;
     CommitArgs ca;
@@ -813,7 +815,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       EvPair f;
       cudaEventCreate(&f.a); cudaEventCreate(&f.b);
       CUDA_TRY(cudaEventRecord(f.a, ps));
-      CUDA_TRY(launch_topk(ca, K, q, d_cands, d_slots, ps));
+      CUDA_TRY(launch_topk(ca, K, q, d_cands, d_slots, d_tkeys, ps));
       CUDA_TRY(launch_propagate(pa, K, ps));
       CUDA_TRY(cudaEventRecord(f.b, ps));
       CUDA_TRY(cudaEventRecord(ev_p, ps));

@@ -896,10 +896,14 @@ cudaError_t launch_build_list(const MarkLayout& L, const uint32_t* mark, uint32_
 // ---- speculative candidate batch (single CTA) ----
 // K-th smallest key among the pixels passing `elig` (radix select, MSB
 // first); returns 0xFFFFFFFE when fewer than K are eligible.
-template <typename Elig>
-__device__ unsigned radix_kth(const CommitArgs& a, unsigned K, Elig elig, unsigned* hist,
+// Keys of the open pixels, computed once per launch with batched loads into a
+// global scratch (4 B per pixel): key = sel_key, ~0 = not eligible.  The
+// radix passes then stream that array (8 loads in flight per thread).
+constexpr int TK_UB = 8;
+
+__device__ unsigned radix_kth(const unsigned* keys, int N, unsigned K, unsigned lim, unsigned* hist,
                               unsigned* shv) {
-  const int N = a.g.N, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   unsigned& s_prefix = shv[0];
   unsigned& s_mask = shv[1];
   unsigned& s_k = shv[2];
@@ -912,28 +916,50 @@ __device__ unsigned radix_kth(const CommitArgs& a, unsigned K, Elig elig, unsign
     __syncthreads();
     const unsigned prefix = s_prefix, mask = s_mask;
     if (!s_all) {
-      for (int v = tid; v < N; v += blockDim.x) {
-        unsigned key;
-        if (!elig(v, key) || (key & mask) != prefix) continue;
-        atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      for (int v0 = tid; v0 < N; v0 += TK_UB * blockDim.x) {
+        unsigned kk[TK_UB];
+#pragma unroll
+        for (int j = 0; j < TK_UB; j++) {
+          const int v = v0 + j * blockDim.x;
+          kk[j] = v < N ? __ldcg(&keys[v]) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int j = 0; j < TK_UB; j++)
+          if (kk[j] != 0xFFFFFFFFu && kk[j] <= lim && (kk[j] & mask) == prefix)
+            atomicAdd(&hist[(kk[j] >> shift) & 255u], 1u);
       }
     }
     __syncthreads();
-    if (tid == 0 && !s_all) {
-      unsigned total = 0;
-      for (int b = 0; b < 256; b++) total += hist[b];
-      if (pass == 0 && total <= s_k) {
-        s_all = 1;
+    if (tid < 32 && !s_all) {  // one warp: scan of the 256 bins
+      const int lane = tid;
+      unsigned c8[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; j++) { c8[j] = hist[lane * 8 + j]; tot += c8[j]; }
+      unsigned incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+      const unsigned kneed = s_k;
+      if (pass == 0 && total <= kneed) {
+        if (lane == 0) s_all = 1;
       } else {
-        unsigned cum = 0;
-        for (int b = 0; b < 256; b++) {
-          if (cum + hist[b] >= s_k) {
-            s_prefix = prefix | ((unsigned)b << shift);
-            s_mask = mask | (255u << shift);
-            s_k -= cum;
-            break;
+        // the bin where the cumulative count first reaches kneed
+        const unsigned excl = incl - tot;
+        if (excl < kneed && kneed <= incl) {
+          unsigned cum = excl;
+          for (int j = 0; j < 8; j++) {
+            if (cum + c8[j] >= kneed) {
+              const unsigned b = (unsigned)(lane * 8 + j);
+              s_prefix = prefix | (b << shift);
+              s_mask = mask | (255u << shift);
+              s_k = kneed - cum;
+              break;
+            }
+            cum += c8[j];
           }
-          cum += hist[b];
         }
       }
     }
@@ -949,30 +975,49 @@ __device__ unsigned radix_kth(const CommitArgs& a, unsigned K, Elig elig, unsign
 // Claims them and hands out tree slots (bump allocator: a pixel is propagated
 // at most once, so N slots always suffice).  The tree becomes visible to the
 // commit loop only when K1 publishes slot_of[src] after writing it.
-__global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int Q, int* cands, int* slots) {
+__global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int Q, int* cands, int* slots,
+                                               unsigned* keys) {
   __shared__ unsigned hist[256];
   __shared__ unsigned shv[4];
   __shared__ int s_n;
   const int N = a.g.N, tid = threadIdx.x;
   if (tid == 0) s_n = 0;
-  unsigned lim = 0xFFFFFFFEu;
-  if (Q > 0) {
-    lim = radix_kth(a, (unsigned)Q, [&](int v, unsigned& key) {
-      key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
-      return key != 0xFFFFFFFFu;
-    }, hist, shv);
+  // keys of all open pixels (kall) and of the unclaimed ones (keys)
+  for (int v0 = tid; v0 < N; v0 += TK_UB * blockDim.x) {
+    int c[TK_UB];
+    uint8_t cl[TK_UB];
+#pragma unroll
+    for (int j = 0; j < TK_UB; j++) {
+      const int v = v0 + j * blockDim.x;
+      c[j] = v < N ? __ldcg(&a.cnt[v]) : 0;
+      cl[j] = v < N ? __ldcg(&a.claimed[v]) : 1;
+    }
+#pragma unroll
+    for (int j = 0; j < TK_UB; j++) {
+      const int v = v0 + j * blockDim.x;
+      if (v >= N) break;
+      const unsigned key = sel_key(a.strategy, N, v, c[j], a.rank);
+      keys[v] = cl[j] ? 0xFFFFFFFFu : key;
+      keys[N + v] = key;
+    }
   }
-  auto unclaimed = [&](int v, unsigned& key) {
-    if (__ldcg(&a.claimed[v])) return false;
-    key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
-    return key != 0xFFFFFFFFu && key <= lim;
-  };
-  const unsigned thr = radix_kth(a, (unsigned)K, unclaimed, hist, shv);
-  for (int v = tid; v < N; v += blockDim.x) {
-    unsigned key;
-    if (!unclaimed(v, key) || key > thr) continue;
-    int i = atomicAdd(&s_n, 1);
-    if (i < K) cands[i] = v;
+  __syncthreads();
+  unsigned lim = 0xFFFFFFFEu;
+  if (Q > 0) lim = radix_kth(keys + N, N, (unsigned)Q, 0xFFFFFFFEu, hist, shv);
+  const unsigned thr = radix_kth(keys, N, (unsigned)K, lim, hist, shv);
+  for (int v0 = tid; v0 < N; v0 += TK_UB * blockDim.x) {
+    unsigned kk[TK_UB];
+#pragma unroll
+    for (int j = 0; j < TK_UB; j++) {
+      const int v = v0 + j * blockDim.x;
+      kk[j] = v < N ? __ldcg(&keys[v]) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int j = 0; j < TK_UB; j++) {
+      if (kk[j] == 0xFFFFFFFFu || kk[j] > lim || kk[j] > thr) continue;
+      const int i = atomicAdd(&s_n, 1);
+      if (i < K) cands[i] = v0 + j * blockDim.x;
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -988,8 +1033,8 @@ __global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int Q, int* 
 }
 
 cudaError_t launch_topk(const CommitArgs& a, int K, int Q, int* cands, int* slots,
-                        cudaStream_t st) {
-  k_topk<<<1, 1024, 0, st>>>(a, K, Q, cands, slots);
+                        unsigned* keys, cudaStream_t st) {
+  k_topk<<<1, 1024, 0, st>>>(a, K, Q, cands, slots, keys);
   return cudaGetLastError();
 }
 

@@ -119,7 +119,7 @@ cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st);
 int commit_max_blocks();
 int commit_fill_depth();
 cudaError_t launch_topk(const CommitArgs& a, int K, int Q, int* cands, int* slots,
-                        cudaStream_t st);
+                        unsigned* keys, cudaStream_t st);
 
 // ---------------- store helpers ----------------
 cudaError_t launch_store_init(const MarkLayout& L, uint32_t* mark, float* D, cudaStream_t st);
