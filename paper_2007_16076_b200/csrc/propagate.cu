@@ -239,10 +239,19 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
       uint32_t lmin = INF_BITS;
       for (int w = tid; w < NW; w += nthr) {
         uint32_t b = vfar[w];
-        while (b) {
-          const int bit = __ffs(b) - 1;
-          b &= b - 1;
-          lmin = min(lmin, vdist[(w << 5) + bit]);
+        while (b) {  // eight far pixels' distances in flight at a time
+          uint32_t dd[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            dd[j] = INF_BITS;
+            if (b) {
+              const int bit = __ffs(b) - 1;
+              b &= b - 1;
+              dd[j] = a.in_smem ? vdist[(w << 5) + bit] : __ldcg(&dist[(w << 5) + bit]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; j++) lmin = min(lmin, dd[j]);
         }
       }
 #pragma unroll
@@ -260,9 +269,21 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
         const uint32_t keep = b;
         uint32_t taken = 0;
         while (b) {
-          const int bit = __ffs(b) - 1;
-          b &= b - 1;
-          if (__uint_as_float(vdist[(w << 5) + bit]) <= thr) taken |= 1u << bit;
+          uint32_t dd[8];
+          int bb[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            bb[j] = -1;
+            dd[j] = INF_BITS;
+            if (b) {
+              bb[j] = __ffs(b) - 1;
+              b &= b - 1;
+              dd[j] = a.in_smem ? vdist[(w << 5) + bb[j]] : __ldcg(&dist[(w << 5) + bb[j]]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            if (bb[j] >= 0 && __uint_as_float(dd[j]) <= thr) taken |= 1u << bb[j];
         }
         if (taken) {
           far[w] = keep & ~taken;
