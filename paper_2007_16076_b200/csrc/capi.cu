@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -41,6 +42,7 @@ struct gp_ctx {
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;  // propagation stream (overlapped with the commit loop)
   cudaStream_t st3 = nullptr;  // device-to-host stream of completed D rows (gp_run_to_host)
+  int border_n = -1;           // border source list resident in the workspace (its length)
   int* h_cnt = nullptr;        // pinned copy of the per-pixel counts
   int nsm = 148;
   // tree store (Euler-tour form) + propagation scratch, lazily sized
@@ -182,7 +184,7 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
 extern "C" int gp_ctx_num_pixels(const gp_ctx* c) { return c ? c->g.N : 0; }
 
 enum { WS_SEQ, WS_NEW, WS_SRC, WS_SLOT_OF, WS_RANK, WS_EXT, WS_SELKEY, WS_FLAGS, WS_CTL, WS_DFC,
-       WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK };
+       WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK, WS_EXTK, WS_EXTT };
 
 template <typename T>
 static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
@@ -300,6 +302,40 @@ static std::vector<int32_t> boundary_pixels(int W, int H) {  // propagation.py:1
 
 // _extrema_context (strategies.py:109-116) on the device; returns the
 // centroid, and fills dfc_dev [N] (device) and the host dist_from_c copy.
+// the two K1 runs of _extrema_context, asynchronous: centroid in d_cen_out
+static int extrema_async(gp_ctx* c, int** d_cen_out, float* dfc_dev) {
+  const int N = c->g.N;
+  std::vector<int32_t> border = boundary_pixels(c->g.W, c->g.H);
+  int* d_src = nullptr;
+  int* d_cen = nullptr;
+  float* d_fb = nullptr;
+  int rc = ensure_scratch(c, 1);
+  if (rc) return rc;
+  CUDA_TRY(ws_get(c, WS_BORDER, &d_src, border.size() + 1));
+  CUDA_TRY(ws_get(c, WS_CEN, &d_cen, 1));
+  CUDA_TRY(ws_get(c, WS_FB, &d_fb, N));
+  if (c->border_n != (int)border.size()) {  // the border list depends only on the shape
+    CUDA_TRY(cudaMemcpyAsync(d_src, border.data(), border.size() * 4, cudaMemcpyHostToDevice, c->st));
+    CUDA_TRY(cudaStreamSynchronize(c->st));
+    c->border_n = (int)border.size();
+  }
+  PropArgs a = base_prop(c);
+  a.src = d_src;
+  a.ns = (int)border.size();
+  a.out_dist = d_fb;
+  a.delta = default_delta(c);
+  CUDA_TRY(launch_propagate(a, 1, c->st));
+  CUDA_TRY(launch_argmax_first(d_fb, N, d_cen, c->st));
+  PropArgs b = base_prop(c);
+  b.src = d_cen;
+  b.ns = 1;
+  b.out_dist = dfc_dev;
+  b.delta = default_delta(c);
+  CUDA_TRY(launch_propagate(b, 1, c->st));
+  *d_cen_out = d_cen;
+  return GP_OK;
+}
+
 static int extrema_device(gp_ctx* c, int* centroid, float* dfc_dev, std::vector<float>& dfc_host) {
   const int N = c->g.N;
   std::vector<int32_t> border = boundary_pixels(c->g.W, c->g.H);
@@ -602,6 +638,16 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   EvPair tot, setup;
   cudaEventCreate(&tot.a); cudaEventCreate(&tot.b);
   cudaEventCreate(&setup.a); cudaEventCreate(&setup.b);
+  const bool htime = getenv("GP_DEBUG_HOST") != nullptr;
+  auto hnow = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double h0 = hnow();
+  std::vector<std::pair<const char*, double>> hmarks;
+  auto hmark = [&](const char* what) {
+    if (!htime) return;
+    const double t = hnow();
+    hmarks.emplace_back(what, t - h0);
+    h0 = t;
+  };
   CUDA_TRY(cudaEventRecord(tot.a, st));
   CUDA_TRY(cudaEventRecord(setup.a, st));
   CUDA_TRY(cudaMemsetAsync(s->cnt, 0, (size_t)N * 4, st));
@@ -654,13 +700,16 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     // the commit kernel leaves on a miss, K1 publishes a tree by writing
     // slot_of[src] after it is complete).  Measured slower on B200 (both roles
     // are latency/issue-bound and contend), so it is off by default.
+    hmark("store reset");
     const bool overlap = getenv("GP_OVERLAP") ? atoi(getenv("GP_OVERLAP")) != 0 : false;
     const int nblocks = commit_blocks(c, overlap);
+    hmark("commit_blocks");
     int uf = N >= 32768 ? 4 : 1;  // work units per commit warp (dynamic balancing)
     if (const char* e = getenv("GP_UNITS_PER_WARP")) uf = std::max(1, atoi(e));
     const int nparts = nblocks * (commit_threads() / 32) * uf;
     int rts = ensure_tree_store(c, nparts);
     if (rts) return rts;
+    hmark("tree store");
     if (!c->st2) CUDA_TRY(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
     cudaStream_t ps = c->st2;
     int *d_slot_of = nullptr, *d_rank = nullptr, *d_ext = nullptr, *d_cands = nullptr;
@@ -704,20 +753,21 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       if (strategy != GP_STRATEGY_FILLING_RATE && !getenv("GP_LIST_ALPHA")) h_ctl.list_switch = 0;
     }
     CUDA_TRY(cudaMemcpyAsync(d_ctl, &h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    hmark("workspace");
+    int* d_cen = nullptr;
     if (strategy == GP_STRATEGY_FILLING_RATE) {
-      int cen = -1;
-      std::vector<float> dfc;
-      int r = extrema_device(c, &cen, d_dfc, dfc);
+      int r = extrema_async(c, &d_cen, d_dfc);
       if (r) return r;
-      std::vector<int32_t> ext, rank(N);
-      ext_order(dfc, ext);
-      for (int i2 = 0; i2 < N; i2++) rank[ext[i2]] = i2;
-      CUDA_TRY(cudaMemcpyAsync(d_rank, rank.data(), N * 4, cudaMemcpyHostToDevice, st));
-      CUDA_TRY(cudaMemcpyAsync(d_ext, ext.data(), N * 4, cudaMemcpyHostToDevice, st));
-      S.centroid = cen;
+      unsigned long long* d_ek = nullptr;
+      unsigned char* d_et = nullptr;
+      const size_t tb = ext_rank_temp_bytes(N);
+      CUDA_TRY(ws_get(c, WS_EXTK, &d_ek, (size_t)2 * N));
+      CUDA_TRY(ws_get(c, WS_EXTT, &d_et, tb));
+      CUDA_TRY(launch_ext_rank(d_dfc, N, d_ek, d_et, tb, d_ext, d_rank, st));
       S.propagations += 2;
-      S.kernels += 3;
+      S.kernels += 6;
     }
+    hmark("extrema+rank enqueued");
     CUDA_TRY(cudaEventRecord(setup.b, st));
     int K = spec_k > 0 ? spec_k : 2 * c->nsm;
     if (spec_k <= 0)
@@ -815,7 +865,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       EvPair f;
       cudaEventCreate(&f.a); cudaEventCreate(&f.b);
       CUDA_TRY(cudaEventRecord(f.a, ps));
-      CUDA_TRY(launch_topk(ca, K, q, d_cands, d_slots, d_tkeys, ps));
+      CUDA_TRY(launch_topk(ca, K, q, d_cands, d_slots, d_tkeys, 0, ps));
       CUDA_TRY(launch_propagate(pa, K, ps));
       CUDA_TRY(cudaEventRecord(f.b, ps));
       CUDA_TRY(cudaEventRecord(ev_p, ps));
@@ -824,12 +874,72 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       S.kernels += 2;
       return GP_OK;
     };
+    const bool pipelined = !overlap && !debug && !(getenv("GP_PIPELINE") && !atoi(getenv("GP_PIPELINE")));
+    if (pipelined) {
+      // Device-gated pipeline: the host enqueues rounds of [commit, top-K,
+      // propagation batch, list switch] on one stream; each kernel checks the
+      // control block and does nothing when its case did not arise (top-K
+      // only after a miss, the switch kernels only after a switch exit, the
+      // commit kernel not after the end), so the GPU never waits for the host.
+      // The host checks the status (and streams finished rows) once per
+      // CHUNK rounds.
+      const unsigned long long lcap = std::max<unsigned long long>(h_ctl.list_switch, 1) + 1024;
+      if (lcap > c->list_cap) {
+        cudaFree(c->list[0]);
+        cudaFree(c->list[1]);
+        c->list[0] = c->list[1] = nullptr;
+        c->list_cap = 0;
+        CUDA_TRY(dalloc(&c->list[0], lcap));
+        CUDA_TRY(dalloc(&c->list[1], lcap));
+        c->list_cap = lcap;
+      }
+      ca.plist[0] = c->list[0];
+      ca.plist[1] = c->list[1];
+      constexpr int CHUNK = 6;
+      auto prop_batch = [&](int gated) -> int {
+        EvPair f;
+        cudaEventCreate(&f.a); cudaEventCreate(&f.b);
+        CUDA_TRY(cudaEventRecord(f.a, st));
+        CUDA_TRY(launch_topk(ca, K, 0, d_cands, d_slots, d_tkeys, gated, st));
+        CUDA_TRY(launch_propagate(pa, K, st));
+        CUDA_TRY(cudaEventRecord(f.b, st));
+        pev.push_back(f);
+        S.kernels += 2;
+        return GP_OK;
+      };
+      hmark("ctx/args");
+      if (int r = prop_batch(0)) return r;
+      hmark("first batch enqueued");
+      for (int guard = 0; guard < 8 * N + 16; guard += CHUNK) {
+        for (int it = 0; it < CHUNK; it++) {
+          EvPair e;
+          cudaEventCreate(&e.a); cudaEventCreate(&e.b);
+          CUDA_TRY(cudaEventRecord(e.a, st));
+          CUDA_TRY(launch_commit(ca, nblocks, st));
+          CUDA_TRY(cudaEventRecord(e.b, st));
+          cev.push_back(e);
+          S.launches++;
+          S.kernels++;
+          if (int r = prop_batch(1)) return r;
+          CUDA_TRY(launch_switch(ca, c->list[0], st));
+          S.kernels += 2;
+        }
+        CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (h_ctl.status == CTL_DONE) break;
+        if (h_ctl.status == CTL_LIMIT) { rc = fail(GP_EINTERNAL, "commit loop stopped unexpectedly"); break; }
+        if (int r = rs.enqueue(false)) return r;  // quiescent: overlaps the next chunk
+      }
+      S.batches = h_ctl.batches;
+    }
     // the first batch must see the initialised workspace on `st`
+    if (!pipelined) {
     CUDA_TRY(cudaStreamSynchronize(st));
     if (int r = batch(0)) return r;
     CUDA_TRY(cudaStreamSynchronize(ps));
     fold_pdbg();
-    for (int guard = 0; guard < 8 * N + 16; guard++) {
+    }
+    for (int guard = 0; !pipelined && guard < 8 * N + 16; guard++) {
       EvPair e;
       cudaEventCreate(&e.a); cudaEventCreate(&e.b);
       CUDA_TRY(cudaEventRecord(e.a, st));
@@ -885,6 +995,12 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     CUDA_TRY(cudaStreamSynchronize(ps));
     CUDA_TRY(cudaEventRecord(tot.b, st));
     CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    if (d_cen) {
+      int cen = -1;
+      CUDA_TRY(cudaMemcpyAsync(&cen, d_cen, 4, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      S.centroid = cen;
+    }
     CUDA_TRY(cudaStreamSynchronize(st));
     if (debug) {
       std::vector<unsigned long long> h((size_t)(N + 2) * 4);
@@ -948,6 +1064,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   }
   S.ms_total = ev_ms(tot);
   S.ms_setup = ev_ms(setup);
+  for (auto& m : hmarks) fprintf(stderr, "[gp host] %-24s %8.3f ms\n", m.first, m.second);
   cudaEventDestroy(tot.a); cudaEventDestroy(tot.b);
   cudaEventDestroy(setup.a); cudaEventDestroy(setup.b);
   if (rc) return rc;

@@ -660,6 +660,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     fq.n = fq.res = fq.head = 0;
   }
   __syncthreads();
+  if (a.ctl->status == CTL_DONE) return;  // pipelined loop: launched past the end
   const int N = a.g.N;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const bool keeper = gtid == 0;  // bookkeeping thread (registers, stores only)
@@ -846,8 +847,8 @@ cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st) 
 }
 
 // ---- list-mode entry: every unfilled pair (u < w) from the mark bitmap ----
-__global__ void k_build_list(MarkLayout L, const uint32_t* mark, uint32_t* list,
-                             unsigned* count) {
+__device__ __forceinline__ void k_build_list_body(MarkLayout L, const uint32_t* mark, uint32_t* list,
+                                                  unsigned* count) {
   const size_t total = (size_t)L.N * L.RW;
   const int lane = threadIdx.x & 31;
   for (size_t b = (size_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b < total;
@@ -885,6 +886,10 @@ __global__ void k_build_list(MarkLayout L, const uint32_t* mark, uint32_t* list,
       list[pos++] = ((uint32_t)u << 16) | (uint32_t)mcol_pixel(L, wbase + bit);
     }
   }
+}
+
+__global__ void k_build_list(MarkLayout L, const uint32_t* mark, uint32_t* list, unsigned* count) {
+  k_build_list_body(L, mark, list, count);
 }
 
 cudaError_t launch_build_list(const MarkLayout& L, const uint32_t* mark, uint32_t* list,
@@ -976,11 +981,15 @@ __device__ unsigned radix_kth(const unsigned* keys, int N, unsigned K, unsigned 
 // at most once, so N slots always suffice).  The tree becomes visible to the
 // commit loop only when K1 publishes slot_of[src] after writing it.
 __global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int Q, int* cands, int* slots,
-                                               unsigned* keys) {
+                                               unsigned* keys, int gated) {
   __shared__ unsigned hist[256];
   __shared__ unsigned shv[4];
   __shared__ int s_n;
   const int N = a.g.N, tid = threadIdx.x;
+  if (gated && a.ctl->status != CTL_MISS) {  // pipelined loop: no batch needed
+    if (tid == 0) a.ctl->ncand = 0;
+    return;
+  }
   if (tid == 0) s_n = 0;
   // keys of all open pixels (kall) and of the unclaimed ones (keys)
   for (int v0 = tid; v0 < N; v0 += TK_UB * blockDim.x) {
@@ -1029,12 +1038,39 @@ __global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int Q, int* 
     }
     c->ncand = n;
     c->total_props += n;
+    c->batches++;
   }
 }
 
 cudaError_t launch_topk(const CommitArgs& a, int K, int Q, int* cands, int* slots,
-                        unsigned* keys, cudaStream_t st) {
-  k_topk<<<1, 1024, 0, st>>>(a, K, Q, cands, slots, keys);
+                        unsigned* keys, int gated, cudaStream_t st) {
+  k_topk<<<1, 1024, 0, st>>>(a, K, Q, cands, slots, keys, gated);
+  return cudaGetLastError();
+}
+
+// Pipelined loop: after a CTL_SWITCH exit, reset the list state and flag the
+// build; the commit kernel that follows runs in list mode.
+__global__ void k_switch_prep(Ctl* ctl) {
+  if (threadIdx.x) return;
+  const int sw = ctl->status == CTL_SWITCH;
+  ctl->build = sw;
+  if (sw) {
+    ctl->list_n[0] = ctl->list_n[1] = 0;
+    ctl->list_cur = 0;
+    ctl->list_dead = 0;
+    ctl->mode = 1;
+    ctl->status = CTL_RUNNING;
+  }
+}
+
+__global__ void k_build_list_gated(MarkLayout L, const uint32_t* mark, uint32_t* list, Ctl* ctl) {
+  if (!*(volatile int*)&ctl->build) return;
+  k_build_list_body(L, mark, list, &ctl->list_n[0]);
+}
+
+cudaError_t launch_switch(const CommitArgs& a, uint32_t* list0, cudaStream_t st) {
+  k_switch_prep<<<1, 32, 0, st>>>(a.ctl);
+  k_build_list_gated<<<148 * 8, 256, 0, st>>>(a.L, a.mark, list0, a.ctl);
   return cudaGetLastError();
 }
 

@@ -64,7 +64,7 @@ struct Ctl {
   int status;     // CTL_*
   int nslots;     // slots ever handed out (bump allocator)
   int ncand;      // candidates produced by the last top-K
-  int pad2;
+  int batches;    // speculative batches that ran (device-gated pipeline)
   int total_props; // trees propagated by speculative batches
   int mode;        // 0: Euler-range fill, 1: unfilled-pair list fill
   unsigned long long visits;  // sum of C over committed trees
@@ -73,6 +73,8 @@ struct Ctl {
   unsigned list_cur;          // live buffer
   unsigned list_dead;         // dead entries in the live buffer
   unsigned long long list_switch;  // switch to list mode when unfilled <= this
+  int build;                       // list build pending (set by k_switch_prep)
+  int pad3;
 };
 enum { CTL_RUNNING = 0, CTL_DONE = 1, CTL_MISS = 2, CTL_LIMIT = 3, CTL_SWITCH = 4 };
 
@@ -119,10 +121,16 @@ cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st);
 int commit_max_blocks();
 int commit_fill_depth();
 cudaError_t launch_topk(const CommitArgs& a, int K, int Q, int* cands, int* slots,
-                        unsigned* keys, cudaStream_t st);
+                        unsigned* keys, int gated, cudaStream_t st);
+// device-gated list switch (pipelined host loop): prep + build only after a CTL_SWITCH exit
+cudaError_t launch_switch(const CommitArgs& a, uint32_t* list0, cudaStream_t st);
 
 // ---------------- store helpers ----------------
 cudaError_t launch_store_init(const MarkLayout& L, uint32_t* mark, float* D, cudaStream_t st);
+// filling-rate ranking on the device (setup.cu): ext / rank from dist_from_c
+size_t ext_rank_temp_bytes(int N);
+cudaError_t launch_ext_rank(const float* dfc, int N, unsigned long long* keys2, void* temp,
+                            size_t temp_bytes, int* ext, int* rank, cudaStream_t st);
 // API-level fills (explicit parent arrays; reference semantics incl. checks)
 cudaError_t launch_fill_tree_api(const MarkLayout& L, const int* parent, const float* tdist,
                                  uint32_t* mark, int* cnt, float* D, unsigned long long* out3,
