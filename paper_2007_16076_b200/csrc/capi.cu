@@ -578,10 +578,31 @@ struct RowStreamer {
   float* host;
   std::vector<uint8_t> sent;
   int64_t rows_sent = 0;
-  int enqueue(bool all) {
+  cudaEvent_t snap_ev = nullptr;
+  bool snap_pending = false;
+  // counts snapshot in stream order (the caller enqueues it at a quiescent
+  // point, then more work); flush() waits for the snapshot only
+  int snapshot() {
+    if (!host) return GP_OK;
+    if (!snap_ev) CUDA_TRY(cudaEventCreateWithFlags(&snap_ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaMemcpyAsync(c->h_cnt, s->cnt, (size_t)c->g.N * 4, cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaEventRecord(snap_ev, c->st));
+    snap_pending = true;
+    return GP_OK;
+  }
+  int flush() {
+    if (!host || !snap_pending) return GP_OK;
+    CUDA_TRY(cudaEventSynchronize(snap_ev));
+    snap_pending = false;
+    return enqueue(false, false);
+  }
+  ~RowStreamer() {
+    if (snap_ev) cudaEventDestroy(snap_ev);
+  }
+  int enqueue(bool all, bool read = true) {
     const int N = c->g.N;
     if (!host) return GP_OK;
-    if (!all) {
+    if (!all && read) {
       CUDA_TRY(cudaMemcpyAsync(c->h_cnt, s->cnt, (size_t)N * 4, cudaMemcpyDeviceToHost, c->st));
       CUDA_TRY(cudaStreamSynchronize(c->st));
     }
@@ -911,6 +932,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       if (int r = prop_batch(0)) return r;
       hmark("first batch enqueued");
       for (int guard = 0; guard < 8 * N + 16; guard += CHUNK) {
+        if (guard) rs.snapshot();  // quiescent point: the previous chunk is complete
         for (int it = 0; it < CHUNK; it++) {
           EvPair e;
           cudaEventCreate(&e.a); cudaEventCreate(&e.b);
@@ -924,11 +946,11 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
           CUDA_TRY(launch_switch(ca, c->list[0], st));
           S.kernels += 2;
         }
+        if (int r = rs.flush()) return r;  // row copies of the last snapshot, during this chunk
         CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
         if (h_ctl.status == CTL_DONE) break;
         if (h_ctl.status == CTL_LIMIT) { rc = fail(GP_EINTERNAL, "commit loop stopped unexpectedly"); break; }
-        if (int r = rs.enqueue(false)) return r;  // quiescent: overlaps the next chunk
       }
       S.batches = h_ctl.batches;
     }
