@@ -73,7 +73,8 @@ def test_l1_distances_exact(gp, oracle):
 @pytest.mark.parametrize("env", [
     {"GP_SPEC_K": "7"}, {"GP_SPEC_K": "1000"}, {"GP_LIST_ALPHA": "0"}, {"GP_LIST_ALPHA": "1000"},
     {"GP_UNITS_PER_WARP": "4"}, {"GP_DELTA_FACTOR": "inf"}, {"GP_DELTA_FACTOR": "0.5"},
-    {"GP_PROP_THREADS": "256"}, {"GP_BARRIER": "sw"},
+    {"GP_PROP_THREADS": "256"}, {"GP_BARRIER": "sw"}, {"GP_PIPELINE": "0"}, {"GP_FILL_QUEUE": "0"},
+    {"GP_FILL_UNROLL": "1"}, {"GP_FILL_UNROLL": "8"}, {"GP_OVERLAP": "1"},
 ])
 def test_tuning_knobs_do_not_change_results(gp, oracle, env, monkeypatch):
     img = np.random.default_rng(11).random((24, 20), dtype=np.float32)
@@ -141,3 +142,15 @@ def test_run_to_host_streams_the_same_array(gp, shape, kind):
     finally:
         L.gp_store_destroy(st)
         L.gp_ctx_destroy(ctx)
+
+
+@pytest.mark.parametrize("pipeline", ["0", "1"])
+def test_run_loops_agree_on_a_larger_image(gp, oracle, pipeline, monkeypatch):
+    """Host-driven and device-gated run loops (many misses, a list switch) vs the oracle."""
+    img = np.random.default_rng(21).random((48, 40), dtype=np.float32)
+    o = oracle.run(img, "filling-rate", nthreads=4)
+    monkeypatch.setenv("GP_PIPELINE", pipeline)
+    monkeypatch.setenv("GP_SPEC_K", "37")
+    run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, gp.StrategyKind.FILLING_RATE)
+    assert _seq(run) == o["seq"].tolist()
+    assert np.array_equal(run.distances.dist, o["D"])
