@@ -4,6 +4,7 @@ Run in the build container (NOT on the GPU box -- /root/reference does not
 exist there):
 
     python tests/golden/make_golden.py small      # reference, tiny images
+    python tests/golden/make_golden.py strategies # reference: spiral / repulsion / extrema runs
     python tests/golden/make_golden.py cfg 2      # reference itself (int config)
     python tests/golden/make_golden.py cfg 4      # reference itself, force=True
     python tests/golden/make_golden.py cfg 1|3|5  # fp32 restatement (oracle/)
@@ -102,6 +103,43 @@ def make_small():
     print("small cases:", cases)
 
 
+def make_strategies():
+    """The other three selectors, run by the reference:
+    sequence, D, counts, adjusted count per image, seed and repulsion."""
+    gp = _ref()
+    rng = np.random.default_rng(16076)
+    out = {}
+    cases = 0
+    kinds = [(gp.StrategyKind.SPIRAL, "spiral"), (gp.StrategyKind.SPIRAL_REPULSION, "repulsion"),
+             (gp.StrategyKind.EXTREMA, "extrema")]
+    for t in range(16):
+        h, w = (int(x) for x in rng.integers(3, 13, 2))
+        img = rng.integers(1, 256, (h, w))
+        if t % 4 == 1:
+            img = rng.integers(1, 4, (h, w))  # tie-heavy
+        metric = gp.Metric.SUM if t % 3 else gp.Metric.MEAN
+        seed = int(rng.integers(0, 1000))
+        rep = 1 + t % 4
+        image = gp.Image(img)
+        k = f"c{cases}_"
+        out[k + "img"] = img.astype(np.int64)
+        out[k + "metric"] = np.array(metric.value)
+        out[k + "seed"] = np.array(seed)
+        out[k + "rep"] = np.array(rep)
+        for kind, tag in kinds:
+            run = gp.run_strategy(image, metric, kind, seed, repulsion=rep)
+            out[k + tag + "_D"] = run.distances.dist
+            out[k + tag + "_seq"] = np.array([s for _, s, _ in run.trace.samples], dtype=np.int64)
+            out[k + tag + "_adj"] = np.array(run.trace.adjusted_count)
+            out[k + tag + "_counts"] = np.array(run.distances.point_filled_counts)
+            out[k + tag + "_rates"] = np.array([[f.numerator, f.denominator] for _, _, f in run.trace.samples],
+                                               dtype=np.int64)
+        cases += 1
+    out["n_cases"] = np.array(cases)
+    np.savez_compressed(os.path.join(HERE, "ref_strategies.npz"), **out)
+    print("strategy cases:", cases)
+
+
 def make_cfg(index: int, nthreads: int):
     spec = CONFIGS[index]
     img = make_image(index)
@@ -154,5 +192,7 @@ def make_cfg(index: int, nthreads: int):
 if __name__ == "__main__":
     if sys.argv[1] == "small":
         make_small()
+    elif sys.argv[1] == "strategies":
+        make_strategies()
     else:
         make_cfg(int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 8)

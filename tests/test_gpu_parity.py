@@ -177,3 +177,28 @@ def test_host_selected_strategies_complete(gp, ref_small):
         run = gp.run_strategy(img, gp.Metric.SUM, kind, seed=0)
         assert run.distances.is_complete
         assert np.array_equal(run.distances.dist, oracle_D), kind
+
+
+def test_other_strategies_match_reference(gp):
+    """Spiral, spiral-repulsion and extrema: host selectors
+    with device propagation and fills vs runs of the reference itself
+    (tests/golden/make_golden.py strategies): sequence, D, counts, adjusted
+    count and the exact filling rates."""
+    from fractions import Fraction
+
+    g = load_golden("ref_strategies.npz")
+    kinds = {"spiral": gp.StrategyKind.SPIRAL, "repulsion": gp.StrategyKind.SPIRAL_REPULSION,
+             "extrema": gp.StrategyKind.EXTREMA}
+    for i in range(int(g["n_cases"])):
+        k = f"c{i}_"
+        img = g[k + "img"]
+        metric = _metric(gp, str(g[k + "metric"]))
+        for tag, kind in kinds.items():
+            run = gp.run_strategy(gp.Image(img), metric, kind, int(g[k + "seed"]), repulsion=int(g[k + "rep"]))
+            seq = [s for _, s, _ in run.trace.samples]
+            assert seq == g[k + tag + "_seq"].tolist(), (i, tag)
+            assert np.array_equal(run.distances.dist, g[k + tag + "_D"]), (i, tag)
+            assert np.array_equal(run.distances.point_filled_counts, g[k + tag + "_counts"]), (i, tag)
+            assert run.trace.adjusted_count == int(g[k + tag + "_adj"]), (i, tag)
+            rates = [Fraction(int(a), int(b)) for a, b in g[k + tag + "_rates"]]
+            assert [f for _, _, f in run.trace.samples] == rates, (i, tag)
