@@ -5,6 +5,7 @@ exist there):
 
     python tests/golden/make_golden.py small      # reference, tiny images
     python tests/golden/make_golden.py strategies # reference: spiral / repulsion / extrema runs
+    python tests/golden/make_golden.py harness    # reference: test images, experiment CSVs
     python tests/golden/make_golden.py cfg 2      # reference itself (int config)
     python tests/golden/make_golden.py cfg 4      # reference itself, force=True
     python tests/golden/make_golden.py cfg 1|3|5  # fp32 restatement (oracle/)
@@ -140,6 +141,29 @@ def make_strategies():
     print("strategy cases:", cases)
 
 
+def make_harness():
+    """Reference test-image families and a small experiment's CSV reports."""
+    gp = _ref()
+    from geopairs.harness import (GeneratorKind, generate_image, hairpin_corridor_mask,
+                                  run_experiment, write_report_csv, write_trace_csv)
+    out = {}
+    sizes = [(25, 25), (12, 9), (7, 16), (31, 20)]
+    for kind in GeneratorKind:
+        for si, size in enumerate(sizes):
+            for seed in (0, 3, 19):
+                out[f"img_{kind.value}_{si}_{seed}"] = generate_image(kind, size, seed).pixels.astype(np.int64)
+    for si, (w, h) in enumerate(sizes):
+        out[f"mask_{si}"] = hairpin_corridor_mask(w, h)
+    images = [(f"{k.value}8", generate_image(k, (8, 7), 5)) for k in GeneratorKind]
+    kinds = [gp.StrategyKind.NAIVE, gp.StrategyKind.SPIRAL, gp.StrategyKind.SPIRAL_REPULSION,
+             gp.StrategyKind.EXTREMA, gp.StrategyKind.FILLING_RATE]
+    rep = run_experiment(images, [gp.Metric.SUM, gp.Metric.MEAN], kinds, [0, 1], verify=True)
+    out["trace_csv"] = np.frombuffer(write_trace_csv(rep.records), dtype=np.uint8)
+    out["report_csv"] = np.frombuffer(write_report_csv(rep), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "ref_harness.npz"), **out)
+    print("harness fixtures:", len(out))
+
+
 def make_cfg(index: int, nthreads: int):
     spec = CONFIGS[index]
     img = make_image(index)
@@ -194,5 +218,7 @@ if __name__ == "__main__":
         make_small()
     elif sys.argv[1] == "strategies":
         make_strategies()
+    elif sys.argv[1] == "harness":
+        make_harness()
     else:
         make_cfg(int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 8)
