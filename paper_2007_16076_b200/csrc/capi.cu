@@ -723,6 +723,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     // are latency/issue-bound and contend), so it is off by default.
     hmark("store reset");
     const bool overlap = getenv("GP_OVERLAP") ? atoi(getenv("GP_OVERLAP")) != 0 : false;
+    commit_configure(overlap ? 0 : N);
     const int nblocks = commit_blocks(c, overlap);
     hmark("commit_blocks");
     int uf = N >= 32768 ? 4 : 1;  // work units per commit warp (dynamic balancing)

@@ -115,6 +115,7 @@ struct CommitArgs {
   unsigned long long total_pairs;
 };
 
+void commit_configure(int N);
 int commit_threads();
 constexpr uint32_t LIST_DEAD = 0xFFFFFFFFu;
 cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st);
