@@ -129,7 +129,7 @@ extern "C" int gp_ctx_create(int H, int W, int dtype, const void* pixels, int me
   int rc = convert_pixels(H, W, dtype, pixels, metric, conn, f, &isint);
   if (rc) return rc;
   gp_ctx* c = new gp_ctx();
-  c->g = Grid{H, W, N, conn, metric};
+  c->g = make_grid(H, W, conn, metric);
   c->isint = isint;
   c->mean_w = mean_weight(f, metric);
   int dev = 0;
@@ -791,7 +791,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     }
     hmark("extrema+rank enqueued");
     CUDA_TRY(cudaEventRecord(setup.b, st));
-    int K = spec_k > 0 ? spec_k : 2 * c->nsm;
+    int K = spec_k > 0 ? spec_k : prop_trees_per_sm(N) * c->nsm;
     if (spec_k <= 0)
       if (const char* e = getenv("GP_SPEC_K")) K = atoi(e);
     K = std::max(1, std::min(K, N));

@@ -26,7 +26,21 @@ constexpr unsigned long long KEY_NONE = ~0ull;
 
 struct Grid {
   int H, W, N, conn, metric;
+  uint32_t wmagic;  // floor(2^32 / W) + 1 (W > 1): exact v / W for v < 2^16
 };
+
+__host__ __device__ inline Grid make_grid(int H, int W, int conn, int metric) {
+  Grid g{H, W, H * W, conn, metric, 0u};
+  if (W > 1) g.wmagic = (uint32_t)((0x100000000ull / (unsigned long long)W) + 1ull);
+  return g;
+}
+
+// row and column of pixel v (N <= 65536, so v * W < 2^32 and the
+// multiply-high quotient is exact)
+__device__ __forceinline__ void pix_rc(const Grid& g, int v, int& r, int& c) {
+  r = g.W > 1 ? (int)__umulhi((uint32_t)v, g.wmagic) : v;
+  c = v - r * g.W;
+}
 
 // scaled_weight (grid.py:146-154) in fp32, no contraction: SUM = 2*fl(a+b).
 __device__ __forceinline__ float edge_w(int metric, float a, float b) {

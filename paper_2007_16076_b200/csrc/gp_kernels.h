@@ -55,6 +55,7 @@ struct PropArgs {
 size_t prop_smem_bytes(int N);
 size_t prop_scratch_bytes(int N);
 bool prop_fits_smem(int N);
+int prop_trees_per_sm(int N);
 cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st);
 
 // ---------------- K2/K3 commit loop ----------------

@@ -44,7 +44,8 @@ namespace gp {
 extern __shared__ __align__(16) unsigned char g_smem[];
 
 constexpr int HIST_SMEM = 4096;  // depth-histogram bins in the shared-memory variant
-constexpr int WL_SMEM = 12288;   // worklist entries kept in smem (global-scratch variant)
+constexpr int HIST_G = 1024;     // depth-histogram bins in smem (global-scratch variant)
+constexpr int WL_SMEM = 9216;    // worklist entries kept in smem (global-scratch variant)
 
 struct PropShared {
   int cnt[2];
@@ -78,6 +79,19 @@ __host__ __device__ inline Layout prop_layout(int N, size_t hist_cap) {
   L.hist = L.inq + bm;
   L.total = L.hist + hist_cap * 4;
   return L;
+}
+
+// Parent codes, 4 bits per pixel in shared memory (window position 0..8,
+// 15 = root): a 256x256 tree's codes take 32 KB, so four trees share an SM.
+__device__ __forceinline__ uint8_t code_get(const volatile uint8_t* code, int v) {
+  const unsigned c = ((unsigned)code[v >> 1] >> ((v & 1) << 2)) & 15u;
+  return c == 15u ? GP_ROOT : (uint8_t)c;
+}
+
+// set the code of a root pixel (nibble 15) to k
+__device__ __forceinline__ void code_attach(volatile uint8_t* code, int v, unsigned k) {
+  unsigned* w = reinterpret_cast<unsigned*>(const_cast<uint8_t*>(code)) + (v >> 3);
+  atomicAnd(w, ~((15u ^ k) << ((v & 7) << 2)));
 }
 
 // u16 array element add via a 32-bit atomic on the containing word
@@ -162,7 +176,8 @@ __device__ void pointer_jump_global(uint32_t* pj, int N) {
   }
 }
 
-__global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
+template <int THR, int MINB>
+__global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   const Grid g = a.g;
   const int N = g.N, NW = (N + 31) >> 5;
   const int t = blockIdx.x;
@@ -173,7 +188,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   unsigned long long* dbg = a.dbg ? a.dbg + (size_t)t * 16 : nullptr;
   if (dbg && tid == 0) { dbg[0] = gtimer(); dbg[12] = 0; dbg[13] = 0; }
 
-  const size_t hist_cap = HIST_SMEM;
+  const size_t hist_cap = a.in_smem ? HIST_SMEM : HIST_G;
   const Layout lay = prop_layout(N, hist_cap);
   unsigned char* base = a.in_smem ? g_smem : a.scratch + (size_t)t * a.scratch_bytes;
   uint32_t* dist = reinterpret_cast<uint32_t*>(base);
@@ -200,7 +215,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     wl.s[1] = wl.s[0] + WL_SMEM;
     wl.cap = WL_SMEM;
     code = g_smem + 2 * bm;
-    hist = reinterpret_cast<uint32_t*>(g_smem + 2 * bm + align16((size_t)N));
+    hist = reinterpret_cast<uint32_t*>(g_smem + 2 * bm + align16((size_t)(N + 1) / 2));
   }
   const float* f = a.in_smem ? fimg : a.img;
   if (a.in_smem)
@@ -340,7 +355,8 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
             int k = idx & 7;
             k += (k >= 4);
             if (k_in_conn(g.conn, k)) {
-              const int r = v / g.W, c = v - r * g.W;
+              int r, c;
+              pix_rc(g, v, r, c);
               uk[j] = nbr_at(g, r, c, k);
               if (uk[j] >= 0) {
                 dvk[j] = __ldcg(&dist[v]);
@@ -380,7 +396,8 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
         int k = idx & 7;
         k += (k >= 4);
         if (k_in_conn(g.conn, k)) {
-          const int r = v / g.W, c = v - r * g.W;
+          int r, c;
+          pix_rc(g, v, r, c);
           u = nbr_at(g, r, c, k);
           if (u >= 0) {
             const float nd = __fadd_rn(__uint_as_float(vdist[v]), edge_w(g.metric, f[v], f[u]));
@@ -420,12 +437,22 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   const size_t off = (size_t)slot * N;
   volatile uint8_t* vcode = code;
   int unparented = 0;
-  for (int v = tid; v < N; v += nthr) {
-    const uint32_t dvb = a.in_smem ? vdist[v] : __ldcg(&dist[v]);
+  // one thread per pixel pair: the two 4-bit codes of a byte are stored together
+  for (int pp = tid; 2 * pp < N; pp += nthr) {
+   unsigned cbyte = 0;
+#pragma unroll 1
+   for (int h = 0; h < 2; h++) {
+    const int v = 2 * pp + h;
     uint8_t cv = GP_ROOT;
+    if (v >= N) {
+      cbyte |= 15u << (4 * h);
+      continue;
+    }
+    const uint32_t dvb = a.in_smem ? vdist[v] : __ldcg(&dist[v]);
     if (!((vfar[v >> 5] >> (v & 31)) & 1u)) {
       const float dv = __uint_as_float(dvb);
-      const int r = v / g.W, c = v - r * g.W;
+      int r, c;
+      pix_rc(g, v, r, c);
       const float fv = f[v];
       uint32_t dub[9];
       float fu[9];
@@ -452,30 +479,33 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
       }
       if (cv == GP_ROOT) unparented = 1;
     }
-    code[v] = cv;
+    cbyte |= (cv == GP_ROOT ? 15u : (unsigned)cv) << (4 * h);
     if (a.out_dist) a.out_dist[off + v] = __uint_as_float(dvb);
+   }
+   code[pp] = (uint8_t)cbyte;
   }
   // zero-weight plateaus (L1 metric only): attach by BFS over tight w=0 edges
   if (__syncthreads_or(unparented)) {
     for (;;) {
       int changed = 0;
       for (int v = tid; v < N; v += nthr) {
-        if (vcode[v] != GP_ROOT || ((vfar[v >> 5] >> (v & 31)) & 1u)) continue;
-        const int r = v / g.W, c = v - r * g.W;
+        if (code_get(vcode, v) != GP_ROOT || ((vfar[v >> 5] >> (v & 31)) & 1u)) continue;
+        int r, c;
+        pix_rc(g, v, r, c);
         for (int k = 0; k < 9; k++) {
           if (!k_in_conn(g.conn, k)) continue;
           const int u = nbr_at(g, r, c, k);
           if (u < 0 || vdist[u] != vdist[v]) continue;
           if (edge_w(g.metric, f[u], f[v]) != 0.0f) continue;
-          const bool attached = vcode[u] != GP_ROOT || ((vfar[u >> 5] >> (u & 31)) & 1u);
-          if (attached) { vcode[v] = (uint8_t)k; changed = 1; break; }
+          const bool attached = code_get(vcode, u) != GP_ROOT || ((vfar[u >> 5] >> (u & 31)) & 1u);
+          if (attached) { code_attach(vcode, v, (unsigned)k); changed = 1; break; }
         }
       }
       if (!__syncthreads_or(changed)) break;
     }
   }
   if (a.out_dir)
-    for (int v = tid; v < N; v += nthr) a.out_dir[off + v] = vcode[v];
+    for (int v = tid; v < N; v += nthr) a.out_dir[off + v] = code_get(vcode, v);
 
   // ---------------- naive epilogue: fill_from_source, row/column x > s ----
   if (a.D) {
@@ -494,7 +524,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   // E1: depths by pointer jumping on packed (depth << 16 | jump) words (A).
   volatile uint32_t* pj = reinterpret_cast<volatile uint32_t*>(base + lay.A);
   for (int v = tid; v < N; v += nthr) {
-    const uint8_t cv = vcode[v];
+    const uint8_t cv = code_get(vcode, v);
     pj[v] = cv == GP_ROOT ? (uint32_t)v : ((1u << 16) | (uint32_t)parent_of(v, cv, g.W));
   }
   __syncthreads();
@@ -589,10 +619,10 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
       const int v0 = vn;
       vn = -1;
       if (d >= 2 && vhist[d - 2] + tid < vhist[d - 1]) vn = order[vhist[d - 2] + tid];
-      if (v0 >= 0) atomic_add_u16(szv, parent_of(v0, vcode[v0], g.W), (unsigned)__ldcg(&szv[v0]) + 1u);
+      if (v0 >= 0) atomic_add_u16(szv, parent_of(v0, code_get(vcode, v0), g.W), (unsigned)__ldcg(&szv[v0]) + 1u);
       for (unsigned i = lo + nthr + tid; i < hi; i += nthr) {
         const int v = order[i];
-        atomic_add_u16(szv, parent_of(v, vcode[v], g.W), (unsigned)__ldcg(&szv[v]) + 1u);
+        atomic_add_u16(szv, parent_of(v, code_get(vcode, v), g.W), (unsigned)__ldcg(&szv[v]) + 1u);
       }
       __syncthreads();
     }
@@ -602,7 +632,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
         const unsigned lo = vhist[d - 1], hi = vhist[d];
         for (unsigned i = lo + lane; i < hi; i += 32) {
           const int v = order[i];
-          atomic_add_u16(szv, parent_of(v, vcode[v], g.W), (unsigned)vszv[v] + 1u);
+          atomic_add_u16(szv, parent_of(v, code_get(vcode, v), g.W), (unsigned)vszv[v] + 1u);
         }
         __syncwarp();
       }
@@ -610,7 +640,7 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
   } else {
     for (int d = maxd; d >= 1; d--) {
       for (int v = tid; v < N; v += nthr)
-        if (depth[v] == d) atomic_add_u16(szv, parent_of(v, vcode[v], g.W), (unsigned)vszv[v] + 1u);
+        if (depth[v] == d) atomic_add_u16(szv, parent_of(v, code_get(vcode, v), g.W), (unsigned)vszv[v] + 1u);
       __syncthreads();
     }
   }
@@ -643,15 +673,16 @@ __global__ void __launch_bounds__(1024, 1) k_propagate(PropArgs a) {
     for (int b = 0; b < 2; b++) {
       const int pp = p0 + b * nthr;
       if (pp >= N) continue;
-      if (vcode[pp] == GP_ROOT) pj[pp] = (uint32_t)pp;
-      const int pr = pp / g.W, pc = pp - pr * g.W;
+      if (code_get(vcode, pp) == GP_ROOT) pj[pp] = (uint32_t)pp;
+      int pr, pc;
+      pix_rc(g, pp, pr, pc);
       // q = pp + offset(k) is a child iff its code points back: code == 8 - k
       const bool interior = pr > 0 && pr < g.H - 1 && pc > 0 && pc < g.W - 1;
 #pragma unroll
       for (int k = 0; k < 9; k++) {
         if (!k_in_conn(g.conn, k)) continue;
         if (!interior && nbr_at(g, pr, pc, k) < 0) continue;
-        if (vcode[pp + (k / 3 - 1) * g.W + (k % 3 - 1)] == (uint8_t)(8 - k)) mask[b] |= 1u << k;
+        if (code_get(vcode, pp + (k / 3 - 1) * g.W + (k % 3 - 1)) == (uint8_t)(8 - k)) mask[b] |= 1u << k;
       }
     }
 #pragma unroll
@@ -869,33 +900,60 @@ size_t prop_scratch_bytes(int N) { return align16(prop_layout(N, (size_t)N + 1).
 
 bool prop_fits_smem(int N) { return prop_smem_bytes(N) <= 227 * 1024; }
 
+// dynamic shared memory of one tree (CTA)
+static size_t prop_dyn_smem(int N) {
+  if (prop_fits_smem(N)) return prop_smem_bytes(N);
+  const size_t bm = align16((size_t)((N + 31) >> 5) * 4);
+  return 2 * bm + std::max((size_t)WL_SMEM * 4, align16((size_t)(N + 1) / 2) + (size_t)HIST_G * 4);
+}
+
+// One tree per CTA.  Trees are latency-bound: two 512-thread CTAs per SM
+// beat one 1024-thread CTA whenever shared memory admits two (128x128 maps
+// need ~212 KB and keep 1024 threads).  The global-scratch variant (52 KB of
+// shared memory) runs three 512-thread CTAs per SM (40 registers, a few
+// spilled): at 256x256 the batch of 444 trees took 731 ms per image against
+// 765 ms for two CTAs per SM; four per SM (32 registers) and four 256-thread
+// CTAs (the same warps over more trees) measured slower.  GP_PROP_MINB=2
+// selects two per SM.
+static int prop_threads(int N) {
+  const size_t per_cta = prop_dyn_smem(N) + 1024 + sizeof(PropShared);
+  int threads = (228 * 1024) / per_cta >= 2 ? 512 : 1024;
+  if (const char* e = getenv("GP_PROP_THREADS")) threads = std::max(128, std::min(1024, atoi(e)));
+  return threads;
+}
+
+static const void* prop_kernel(int N, int threads) {
+  const size_t per_cta = prop_dyn_smem(N) + 1024 + sizeof(PropShared);
+  int minb = 3;
+  if (const char* e = getenv("GP_PROP_MINB")) minb = atoi(e);
+  if (!prop_fits_smem(N) && threads == 512 && minb == 3 && (228 * 1024) / per_cta >= 3)
+    return (const void*)k_propagate<512, 3>;
+  return (const void*)k_propagate<1024, 1>;
+}
+
+// speculative batch size per SM: the concurrent trees of the global-scratch
+// variant; two otherwise (measured on 64x64 and 128x128 maps)
+int prop_trees_per_sm(int N) {
+  if (prop_fits_smem(N)) return 2;
+  const int threads = prop_threads(N);
+  const void* k = prop_kernel(N, threads);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prop_dyn_smem(N));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, prop_dyn_smem(N));
+  return std::max(1, per_sm);
+}
+
 cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st) {
   if (ntrees <= 0) return cudaSuccess;
-  size_t smem = 0;
   a.in_smem = prop_fits_smem(a.g.N) ? 1 : 0;
-  if (a.in_smem) {
-    smem = prop_smem_bytes(a.g.N);
-    cudaError_t e = cudaFuncSetAttribute(k_propagate, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-  } else {
-    a.scratch_bytes = prop_scratch_bytes(a.g.N);
-    const int NW = (a.g.N + 31) >> 5;
-    smem = 2 * align16((size_t)NW * 4) +
-           std::max((size_t)WL_SMEM * 4, align16((size_t)a.g.N) + (size_t)HIST_SMEM * 4);
-    cudaError_t e = cudaFuncSetAttribute(k_propagate, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  // One tree per CTA.  Trees are latency-bound, so two 512-thread CTAs per SM
-  // beat one 1024-thread CTA whenever shared memory admits two (registers:
-  // 2 x 512 x <=64); 128x128 maps need ~212 KB and keep 1024 threads.
-  const size_t per_cta = smem + 1024 + sizeof(PropShared);
-  int threads = (228 * 1024) / per_cta >= 2 ? 512 : 1024;
-  if (a.threads) threads = a.threads;
-  if (const char* e = getenv("GP_PROP_THREADS")) threads = std::max(128, std::min(1024, atoi(e)));
-  k_propagate<<<ntrees, threads, smem, st>>>(a);
-  return cudaGetLastError();
+  if (!a.in_smem) a.scratch_bytes = prop_scratch_bytes(a.g.N);
+  const size_t smem = prop_dyn_smem(a.g.N);
+  const int threads = a.threads ? a.threads : prop_threads(a.g.N);
+  const void* kern = prop_kernel(a.g.N, threads);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  void* params[] = {&a};
+  return cudaLaunchKernel(kern, dim3(ntrees), dim3(threads), params, smem, st);
 }
 
 }  // namespace gp
