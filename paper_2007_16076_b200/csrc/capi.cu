@@ -867,10 +867,11 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     if (debug) {
       CUDA_TRY(dalloc(&d_pdbg, (size_t)K * 16));
       pa.dbg = d_pdbg;
-      CUDA_TRY(dalloc(&d_cdbg, (size_t)(N + 2) * 16));
-      CUDA_TRY(cudaMemsetAsync(d_cdbg, 0, (size_t)(N + 2) * 128, st));
+      CUDA_TRY(dalloc(&d_cdbg, (size_t)(N + 2) * 17));
+      CUDA_TRY(cudaMemsetAsync(d_cdbg, 0, (size_t)(N + 2) * 136, st));
       ca.dbg = d_cdbg;
       ca.dbgw = d_cdbg + (size_t)(N + 2) * 4;
+      ca.dbgo = d_cdbg + (size_t)(N + 2) * 16;
       if (getenv("GP_DEBUG_SIM")) ca.dbgs = d_cdbg + (size_t)(N + 2) * 8;
       if (const char* e = getenv("GP_DEBUG_UNITS")) {
         ca.dbgu_step = atoi(e);
@@ -1032,17 +1033,19 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
         std::vector<unsigned long long> nw2(h_ctl.step), hw((size_t)(N + 2) * 4);
         cudaMemcpy(nw2.data(), d_new, (size_t)h_ctl.step * 8, cudaMemcpyDeviceToHost);
         cudaMemcpy(hw.data(), ca.dbgw, hw.size() * 8, cudaMemcpyDeviceToHost);
-        std::vector<unsigned long long> hs((size_t)(N + 2) * 8, 0);
+        std::vector<unsigned long long> hs((size_t)(N + 2) * 8, 0), ho((size_t)(N + 2), 0), hk((size_t)(N + 2), 0);
         if (ca.dbgs) cudaMemcpy(hs.data(), ca.dbgs, hs.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(ho.data(), ca.dbgo, ho.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(hk.data(), d_selkey, hk.size() * 8, cudaMemcpyDeviceToHost);
         const int nwarps = nblocks * (commit_threads() / 32);
         if (FILE* fp = fopen(path, "w")) {
           for (int i2 = 0; i2 < h_ctl.step; i2++) {
             unsigned long long* r = &h[(size_t)i2 * 4];
             const unsigned long long* q = &hs[(size_t)i2 * 8];
-            fprintf(fp, "%d %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i2,
+            fprintf(fp, "%d %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", i2,
                     r[0], r[1], r[2], r[3], nw2[i2], hw[(size_t)i2 * 4], hw[(size_t)i2 * 4 + 1] / (unsigned long long)nwarps,
                     q[0], q[1], q[2], q[3], hw[(size_t)i2 * 4 + 2], hw[(size_t)i2 * 4 + 3] / (unsigned long long)nblocks,
-                    q[4], q[5], q[6], q[7]);
+                    q[4], q[5], q[6], q[7], ho[i2], hk[i2] >> 48);
           }
           fclose(fp);
         }

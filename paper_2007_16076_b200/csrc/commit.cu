@@ -95,10 +95,17 @@ __device__ __forceinline__ unsigned long long sel_pack(unsigned key, int v, int 
 __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned long long* red64) {
   const int N = a.g.N;
   unsigned long long m = ~0ull;
+  unsigned nopen = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
     if (v == skip) continue;
     const unsigned key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
     if (key != 0xFFFFFFFFu) m = min(m, sel_pack(key, v, __ldcg(&a.slot_of[v])));
+    nopen += key != 0xFFFFFFFFu;
+  }
+  if (a.dbgo) {  // debug: open pixels after the previous commit
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nopen += __shfl_xor_sync(0xffffffffu, nopen, o);
+    if ((threadIdx.x & 31) == 0 && nopen) atomicAdd(&a.dbgo[step], (unsigned long long)nopen);
   }
   m = block_reduce_min(m, red64);
   if (threadIdx.x == 0 && m != ~0ull) atomicMin(&a.selkey[step], m);
@@ -585,7 +592,10 @@ __device__ __forceinline__ void grid_barrier(GridBarrier* bar, unsigned& gen) {
 // are in flight together.
 constexpr int LU = 4;
 __device__ __forceinline__ unsigned fill_list(const CommitArgs& a, int slot, int s,
-                                              unsigned cur, unsigned n) {
+                                              unsigned cur, unsigned n,
+                                              unsigned long long* prb = nullptr) {
+  const unsigned long long tp0 = prb ? gtimer() : 0ull;
+  unsigned long long tp1 = 0, tp2 = 0;
   const int N = a.g.N;
   const size_t off = (size_t)slot * N;
   const uint32_t* tinz = a.ts.tin + off;
@@ -609,6 +619,12 @@ __device__ __forceinline__ unsigned fill_list(const CommitArgs& a, int slot, int
         zw[j] = __ldg(&tinz[e[j] & 0xFFFFu]);
       }
     }
+    if (prb && !tp1) {  // debug: first round's entry loads and tree gathers
+      asm volatile("" ::"r"(e[0]), "r"(e[LU - 1]));
+      tp1 = gtimer();
+      asm volatile("" ::"r"(zu[0]), "r"(zw[0]), "r"(zu[LU - 1]), "r"(zw[LU - 1]));
+      tp2 = gtimer();
+    }
 #pragma unroll
     for (int j = 0; j < LU; j++) {
       if (e[j] == LIST_DEAD) continue;
@@ -629,6 +645,13 @@ __device__ __forceinline__ unsigned fill_list(const CommitArgs& a, int slot, int
       list[i0 + j * stride] = LIST_DEAD;
       mine++;
     }
+  }
+  if (prb && (threadIdx.x & 31) == 0 && tp1) {
+    const unsigned long long t3 = gtimer();
+    atomicMax(&prb[0], tp1 - tp0);
+    atomicMax(&prb[1], tp2 - tp0);
+    atomicMax(&prb[2], t3 - tp0);
+    if (mine) atomicMax(&prb[3], t3 - tp0);
   }
   return mine;
 }
@@ -706,7 +729,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     // ---- K2: fill ----
     unsigned long long lnew = 0;
     if (mode == 1) {
-      lnew = fill_list(a, slot, s, lcur, ln);
+      lnew = fill_list(a, slot, s, lcur, ln, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr);
     } else if (a.fillq) {
       lnew = fill_tree_cta<G>(a, slot, s, fq, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr);
     } else {

@@ -111,6 +111,7 @@ struct CommitArgs {
   int fillq;                // tree-mode fill through the per-CTA chunk queue (default 1)
   unsigned* dbgu;           // optional per-unit stats of step dbgu_step (GP_DEBUG_UNITS)
   int dbgu_step;
+  unsigned long long* dbgo; // optional per-step open-pixel counts (debug dump)
   GridBarrier* bar;
   uint32_t* plist[2];      // unfilled pairs (u << 16 | w, u < w), list mode
   unsigned long long total_pairs;

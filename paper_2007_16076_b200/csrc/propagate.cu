@@ -331,16 +331,21 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
     items_total += n;
     // the current items leave the queue: improvements from now on re-queue them
     for (int i = tid; i < n; i += nthr) {
-      const int v = *wl.at(cur, i);
+      const int v = i < wl.cap ? (int)wl.s[cur][i] : (int)*wl.at(cur, i);
       atomicAnd(&inq[v >> 5], ~(1u << (v & 31)));
     }
     if (tid == 0) sh.cnt[cur ^ 1] = 0;
     __syncthreads();
     if (!a.in_smem) {
       // global variant: RR rounds of (item, edge) pairs per thread in flight
-      // together -- distance loads, then independent atomics at L2
+      // together -- distance loads, then independent atomics at L2.  The
+      // worklist is read from shared memory directly while it fits there; the
+      // window offsets come from packed constants, one unsigned compare per
+      // bound; the appends of the RR rounds share one counter update.
       constexpr int RR = 4;
       const int items = n * 8;
+      const bool wl_fits = n <= wl.cap;
+      const uint16_t* lsm = wl.s[cur];
       for (int b0 = 0; b0 < items; b0 += RR * nthr) {
         int uk[RR];
         uint32_t nbk[RR], oldk[RR], dvk[RR];
@@ -351,14 +356,17 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
           uk[j] = -1;
           dvk[j] = INF_BITS;
           if (idx < items) {
-            const int v = *wl.at(cur, idx >> 3);
+            const int it = idx >> 3;
+            const int v = wl_fits ? (int)lsm[it] : (int)*wl.at(cur, it);
             int k = idx & 7;
             k += (k >= 4);
             if (k_in_conn(g.conn, k)) {
               int r, c;
               pix_rc(g, v, r, c);
-              uk[j] = nbr_at(g, r, c, k);
-              if (uk[j] >= 0) {
+              const int dr = (int)((0x2A540u >> (2 * k)) & 3u) - 1;  // k / 3 - 1
+              const int dc = (int)((0x24924u >> (2 * k)) & 3u) - 1;  // k % 3 - 1
+              if ((unsigned)(r + dr) < (unsigned)g.H && (unsigned)(c + dc) < (unsigned)g.W) {
+                uk[j] = v + dr * g.W + dc;
                 dvk[j] = __ldcg(&dist[v]);
                 fwk[j] = edge_w(g.metric, __ldg(&f[v]), __ldg(&f[uk[j]]));
               }
@@ -370,16 +378,31 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
           nbk[j] = uk[j] >= 0 ? __float_as_uint(__fadd_rn(__uint_as_float(dvk[j]), fwk[j])) : INF_BITS;
           oldk[j] = uk[j] >= 0 ? atomicMin(&dist[uk[j]], nbk[j]) : 0u;
         }
+        bool app[RR];
+        unsigned mj[RR];
+        int tot = 0;
 #pragma unroll
         for (int j = 0; j < RR; j++) {
-          bool app = false;
+          app[j] = false;
           const int u = uk[j];
           if (u >= 0 && nbk[j] < oldk[j]) {
             const uint32_t ub = 1u << (u & 31);
-            if (__uint_as_float(nbk[j]) <= thr) app = !(atomicOr(&inq[u >> 5], ub) & ub);
+            if (__uint_as_float(nbk[j]) <= thr) app[j] = !(atomicOr(&inq[u >> 5], ub) & ub);
             else atomicOr(&far[u >> 5], ub);
           }
-          warp_append(app, u, &sh.cnt[cur ^ 1], wl, cur ^ 1);
+          mj[j] = __ballot_sync(0xffffffffu, app[j]);
+          tot += __popc(mj[j]);
+        }
+        if (tot) {  // warp-uniform
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&sh.cnt[cur ^ 1], tot);
+          base = __shfl_sync(0xffffffffu, base, 0);
+          const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+          for (int j = 0; j < RR; j++) {
+            if (app[j]) *wl.at(cur ^ 1, base + __popc(mj[j] & lt)) = (uint16_t)uk[j];
+            base += __popc(mj[j]);
+          }
         }
       }
       cur ^= 1;
