@@ -88,10 +88,13 @@ __device__ __forceinline__ uint8_t code_get(const volatile uint8_t* code, int v)
   return c == 15u ? GP_ROOT : (uint8_t)c;
 }
 
-// set the code of a root pixel (nibble 15) to k
-__device__ __forceinline__ void code_attach(volatile uint8_t* code, int v, unsigned k) {
+// set the code of pixel v to k (the other nibbles of the word may change
+// concurrently: both steps are atomic)
+__device__ __forceinline__ void code_set(volatile uint8_t* code, int v, unsigned k) {
   unsigned* w = reinterpret_cast<unsigned*>(const_cast<uint8_t*>(code)) + (v >> 3);
-  atomicAnd(w, ~((15u ^ k) << ((v & 7) << 2)));
+  const int sh = (v & 7) << 2;
+  atomicOr(w, 15u << sh);
+  atomicAnd(w, ~((15u ^ k) << sh));
 }
 
 // u16 array element add via a 32-bit atomic on the containing word
@@ -507,25 +510,62 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
    }
    code[pp] = (uint8_t)cbyte;
   }
-  // zero-weight plateaus (L1 metric only): attach by BFS over tight w=0 edges
+  // Zero-weight plateaus (L1 metric only).  A pixel without a tight neighbour
+  // of smaller (d, id) is a local root, and pixels parented so far may hang
+  // off one, so "has a parent" does not mean "reaches a source".  Connected
+  // pixels (chain reaches a source) grow breadth-first from the sources in
+  // synchronous sweeps: an unconnected pixel joins when its parent is
+  // connected, else it is re-parented to its first connected tight neighbour
+  // (window order); decisions of a sweep read only the previous sweep's set
+  // (`inq`, zero after the relaxation; new members collect in `far`, whose
+  // root marks are no longer needed), so the forest is deterministic.  Every
+  // pixel has a tight neighbour on a shortest path from a source, so the
+  // sweeps connect all pixels; parents are always connected, so no cycles.
   if (__syncthreads_or(unparented)) {
+    volatile uint32_t* vcon = inq;
+    for (int i = tid; i < NW; i += nthr) far[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < a.ns; i += nthr) {
+      const int v = my_src[i];
+      atomicOr(&inq[v >> 5], 1u << (v & 31));
+    }
+    __syncthreads();
     for (;;) {
       int changed = 0;
       for (int v = tid; v < N; v += nthr) {
-        if (code_get(vcode, v) != GP_ROOT || ((vfar[v >> 5] >> (v & 31)) & 1u)) continue;
+        if ((vcon[v >> 5] >> (v & 31)) & 1u) continue;
+        const uint8_t cv = code_get(vcode, v);
+        if (cv != GP_ROOT) {
+          const int p = parent_of(v, cv, g.W);
+          if ((vcon[p >> 5] >> (p & 31)) & 1u) {
+            atomicOr(&far[v >> 5], 1u << (v & 31));
+            changed = 1;
+            continue;
+          }
+        }
         int r, c;
         pix_rc(g, v, r, c);
+        const float dv = __uint_as_float(vdist[v]);
         for (int k = 0; k < 9; k++) {
           if (!k_in_conn(g.conn, k)) continue;
           const int u = nbr_at(g, r, c, k);
-          if (u < 0 || vdist[u] != vdist[v]) continue;
-          if (edge_w(g.metric, f[u], f[v]) != 0.0f) continue;
-          const bool attached = code_get(vcode, u) != GP_ROOT || ((vfar[u >> 5] >> (u & 31)) & 1u);
-          if (attached) { code_attach(vcode, v, (unsigned)k); changed = 1; break; }
+          if (u < 0 || !((vcon[u >> 5] >> (u & 31)) & 1u)) continue;
+          if (__fadd_rn(__uint_as_float(vdist[u]), edge_w(g.metric, f[u], f[v])) != dv) continue;
+          code_set(vcode, v, (unsigned)k);
+          atomicOr(&far[v >> 5], 1u << (v & 31));
+          changed = 1;
+          break;
         }
       }
       if (!__syncthreads_or(changed)) break;
+      for (int i = tid; i < NW; i += nthr) {
+        inq[i] |= far[i];
+        far[i] = 0;
+      }
+      __syncthreads();
     }
+    for (int i = tid; i < NW; i += nthr) inq[i] = 0;
+    __syncthreads();
   }
   if (a.out_dir)
     for (int v = tid; v < N; v += nthr) a.out_dir[off + v] = code_get(vcode, v);

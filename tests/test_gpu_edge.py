@@ -68,13 +68,27 @@ def test_l1_distances_exact(gp, oracle):
             p = int(r.parent[v])
             if p >= 0:
                 assert r.dist[v] == r.dist[p] + gp.edge_weight(gp.Image(img), gp.Metric.L1, p, v)
+        _check_tree(np.asarray(r.dist, dtype=np.float32), r.parent, img, 8, "l1", [s])
+
+
+@pytest.mark.parametrize("shape", [(8, 9), (21, 17)])
+def test_l1_plateau_run_completes_with_exact_distances(gp, oracle, shape):
+    """L1 on a plateau image: trees are not pinned to the heap order, but each
+    is a shortest-path tree, so the completed array equals the brute-force
+    distances exactly (integer image)."""
+    img = np.random.default_rng(12).integers(1, 4, shape) * 5
+    brute = oracle.run(img, "naive", metric="l1")["D"]
+    for kind in (gp.StrategyKind.FILLING_RATE, gp.StrategyKind.NAIVE):
+        run = gp.run_strategy(gp.Image(img), gp.Metric.L1, kind)
+        assert run.distances.is_complete
+        assert np.array_equal(run.distances.dist, brute)
 
 
 @pytest.mark.parametrize("env", [
     {"GP_SPEC_K": "7"}, {"GP_SPEC_K": "1000"}, {"GP_LIST_ALPHA": "0"}, {"GP_LIST_ALPHA": "1000"},
     {"GP_UNITS_PER_WARP": "4"}, {"GP_DELTA_FACTOR": "inf"}, {"GP_DELTA_FACTOR": "0.5"},
     {"GP_PROP_THREADS": "256"}, {"GP_BARRIER": "sw"}, {"GP_PIPELINE": "0"}, {"GP_FILL_QUEUE": "0"},
-    {"GP_FILL_UNROLL": "1"}, {"GP_FILL_UNROLL": "8"}, {"GP_OVERLAP": "1"},
+    {"GP_FILL_UNROLL": "1"}, {"GP_FILL_UNROLL": "8"}, {"GP_OVERLAP": "1"}, {"GP_PROP_MINB": "2"},
 ])
 def test_tuning_knobs_do_not_change_results(gp, oracle, env, monkeypatch):
     img = np.random.default_rng(11).random((24, 20), dtype=np.float32)
@@ -154,3 +168,65 @@ def test_run_loops_agree_on_a_larger_image(gp, oracle, pipeline, monkeypatch):
     run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, gp.StrategyKind.FILLING_RATE)
     assert _seq(run) == o["seq"].tolist()
     assert np.array_equal(run.distances.dist, o["D"])
+
+
+def _check_tree(dist, parent, img, conn, metric, sources):
+    """parent is a valid shortest-path forest of dist (zero-weight plateaus)."""
+    H, W = img.shape
+    f = img.astype(np.float32).ravel()
+    N = H * W
+    roots = set(int(s) for s in sources)
+    for v in range(N):
+        p = int(parent[v])
+        if v in roots:
+            assert p == -1
+            continue
+        dr, dc = p // W - v // W, p % W - v % W
+        assert max(abs(dr), abs(dc)) == 1 and (conn == 8 or abs(dr) + abs(dc) == 1)
+        a, b = np.float32(f[p]), np.float32(f[v])
+        w = {"sum": np.float32(2) * (a + b), "mean": a + b, "l1": np.float32(2) * abs(a - b)}[metric]
+        assert np.float32(dist[p] + w) == dist[v]
+    # acyclic: every chain reaches a root within N steps
+    done = np.zeros(N, dtype=bool)
+    for v in range(N):
+        chain, x = [], v
+        while not done[x] and parent[x] >= 0:
+            chain.append(x)
+            x = int(parent[x])
+            assert len(chain) <= N, "parent cycle"
+        assert parent[x] >= 0 or x in roots or done[x]
+        done[chain] = True
+        done[x] = True
+
+
+@pytest.mark.parametrize("shape,conn,metric,isint", [
+    ((150, 140), 8, "sum", False),
+    ((150, 140), 4, "sum", False),
+    ((131, 160), 8, "mean", True),
+    ((256, 256), 8, "sum", False),
+    ((64, 1024), 8, "sum", True),
+    ((160, 120), 8, "l1", True),
+])
+def test_global_scratch_propagation_matches_oracle(gp, oracle, shape, conn, metric, isint):
+    """Maps above the shared-memory limit run K1's global-scratch variant
+    (three trees per SM, 4-bit parent codes): distances bit-exact, parents
+    identical (positive weights) or a valid shortest-path tree (L1 plateaus)."""
+    rng = np.random.default_rng(sum(shape) + conn)
+    if isint:
+        img = rng.integers(1, 256, shape)
+        if metric == "l1":
+            img = (img // 64 + 1) * 10  # plateaus: zero-weight edges
+    else:
+        img = rng.random(shape, dtype=np.float32)
+    m = {"sum": gp.Metric.SUM, "mean": gp.Metric.MEAN, "l1": gp.Metric.L1}[metric]
+    graph = gp.GridGraph(gp.Image(img), m, connectivity=conn)
+    N = shape[0] * shape[1]
+    srcs = [0, N - 1, N // 2 + shape[1] // 3] + [int(x) for x in rng.choice(N, 2, replace=False)]
+    for s in srcs:
+        r = graph.propagate([s])
+        d, p = oracle.propagate(img, [s], conn=conn, metric=metric)
+        assert np.array_equal(np.asarray(r.dist), d), s
+        if metric != "l1":
+            assert np.array_equal(r.parent, p), s
+        else:
+            _check_tree(np.asarray(r.dist, dtype=np.float32), r.parent, img, conn, metric, [s])
