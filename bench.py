@@ -112,6 +112,23 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def _traffic(config: int, kernel: str):
+    """DRAM bytes (read + write) of `kernel` summed over one image's launches,
+    from the newest committed ncu capture profiles/*_cfg<config>_traffic.json
+    (scripts/ncu_traffic.py); None when there is none."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_cfg{config}_traffic.json")))
+    if not files:
+        return None, None
+    try:
+        with open(files[-1]) as f:
+            k = json.load(f)["kernels"][kernel]
+        return k, os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 def _cpu_sample(img, spec, target_s: float, nthreads: int):
     """The oracle port's real loop (selection + propagation + fill) for the
     first M commits of the run, timed inside the loop (allocation excluded)."""
@@ -307,6 +324,8 @@ def main():
     if spec.strategy == "naive":
         b_alg = 4.0 * N * N + N * N / 8.0 + 10.0 * N * P
         achieved = b_alg / (prop_ms / 1e3) / 1e9
+    kname = "k_commit" if spec.strategy != "naive" else "k_propagate"
+    tk, tsrc = _traffic(args.config, kname)
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -320,8 +339,13 @@ def main():
         "e2e": {"value": world * A / e2e_s, "unit": "pairs/s", "ms_per_image": e2e_s * 1e3,
                 "h2d_bytes_per_step": int(px.nbytes), "d2h_bytes_per_step": 4 * N * N},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "k_commit" if spec.strategy != "naive" else "k_propagate",
+                     "frac": achieved / peak, "traffic": tk["dram_bytes"] if tk else None,
+                     "traffic_scope": (f"bytes per image: ncu dram__bytes_read.sum + dram__bytes_write.sum "
+                                       f"summed over the {tk['launches']} {kname} launches of one image "
+                                       f"({tsrc}); achieved uses the same per-image scope") if tk else None,
+                     "traffic_per_launch": tk["dram_bytes_per_launch"] if tk else None,
+                     "traffic_over_algorithmic": tk["dram_bytes"] / b_alg if tk else None,
+                     "peak_kind": peak_kind, "kernel": kname,
                      "algorithmic_bytes_per_image": b_alg, "C_visits": C,
                      "kernel_ms_per_image": commit_ms if spec.strategy != "naive" else prop_ms},
         "breakdown_ms": {"commit": commit_ms, "propagate": prop_ms,

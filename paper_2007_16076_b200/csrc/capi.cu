@@ -833,6 +833,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     pa.ts = c->ts;
     pa.L = L;
     pa.publish = d_slot_of;
+    pa.list_mode = &d_ctl->mode;  // trees made after the list switch skip pre/szp/partition
     pa.delta = default_delta(c);
     pa.threads = overlap ? 512 : 0;
     const bool debug = getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"));

@@ -50,6 +50,7 @@ struct PropArgs {
   unsigned long long* dbg; // optional per-tree phase stamps [ntrees][8] (debug)
   int* publish;            // optional slot_of[]: set slot_of[src] = slot once the tree is written
   int threads;             // CTA size override (0: automatic)
+  const int* list_mode;    // optional &Ctl::mode: == 1 -> list-mode tree (tin/tdp/C only)
 };
 
 size_t prop_smem_bytes(int N);

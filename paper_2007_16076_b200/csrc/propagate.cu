@@ -56,6 +56,7 @@ struct PropShared {
   unsigned total;
   unsigned pairs;
   int nbig;
+  int lite;  // list-mode tree: tin/tdp/C only (no pre/szp/partition)
 };
 
 struct Layout {
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
     sh.cnt[1] = 0;
     sh.maxd = 0;
     sh.pairs = 0;
+    sh.lite = a.list_mode ? (*(volatile const int*)a.list_mode == 1) : 0;
   }
   __syncthreads();
   const int* my_src = a.src + (size_t)t * a.ns;
@@ -607,7 +609,9 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   constexpr int UB = 8;
   // E2: depth (B) and max depth
   volatile uint16_t* depth = reinterpret_cast<volatile uint16_t*>(base + lay.B);
+  // C = ancestor/descendant pairs of the tree = sum of depths
   int lmax = 0;
+  unsigned lpairs = 0;
   for (int v0 = tid; v0 < N; v0 += UB * nthr) {
     uint32_t x[UB];
 #pragma unroll
@@ -618,9 +622,11 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       const int d = (int)(x[j] >> 16);
       depth[v0 + j * nthr] = (uint16_t)d;
       lmax = max(lmax, d);
+      lpairs += (unsigned)d;
     }
   }
   atomicMax(&sh.maxd, lmax);
+  atomicAdd(&sh.pairs, lpairs);
   __syncthreads();
   const int maxd = sh.maxd;
   if (dbg && tid == 0) { dbg[8] = gtimer(); dbg[11] = maxd; }
@@ -772,6 +778,10 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   if (a.in_smem) pointer_jump(pj, N);
   else pointer_jump_global(const_cast<uint32_t*>(pj), N);
   if (dbg && tid == 0) dbg[4] = gtimer();
+  // Tree-store outputs are written with evict-first stores (st.global.cs): the
+  // commit loop reads a tree long after it is written, and streaming ~1 MB per
+  // tree through L2 with normal priority evicts the scratch of the trees
+  // still being built.
   // E6: preorder arrays.  tdp straight to global, then pre/szp staged in the
   // (now free) distance region for coalesced stores and the partition scan.
   // The arrays read here are stable after the barriers: the global variant
@@ -794,11 +804,21 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       const int v = v0 + j * nthr;
       if (v >= N) break;
       const uint32_t q = x[j] >> 16;
-      gtdp[q] = __uint_as_float(dv[j]);
-      gtin[v] = q | ((uint32_t)sz[j] << 16);
+      __stcs(&gtdp[q], __uint_as_float(dv[j]));
+      __stcs(&gtin[v], q | ((uint32_t)sz[j] << 16));
     }
   }
   __syncthreads();
+  const int slot_c = slot;
+  if (sh.lite) {
+    // list mode (the commit loop only tests Euler intervals from now on):
+    // tin and tdp are all it reads
+    if (tid == 0) {
+      a.ts.T[slot_c] = 0;
+      a.ts.C[slot_c] = sh.pairs;
+      if (dbg) dbg[15] = dbg[5] = gtimer();
+    }
+  } else {
   volatile uint16_t* preS = reinterpret_cast<volatile uint16_t*>(base);
   volatile uint16_t* szS = preS + N;
   for (int v0 = tid; v0 < N; v0 += UE * nthr) {
@@ -834,8 +854,8 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
     for (int j = 0; j < UB; j++) {
       const int q = q0 + j * nthr;
       if (q >= N) break;
-      gpre[q] = (mcol(ML, pv[j]) << 16) | pv[j];
-      gszp[q] = sz[j];
+      __stcs(&gpre[q], (mcol(ML, pv[j]) << 16) | pv[j]);
+      __stcs(&gszp[q], (unsigned short)sz[j]);
     }
   }
   if (dbg) {
@@ -845,7 +865,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   // E7: chunk counts ceil(szp/32), exclusive scan over preorder, partition
   const int seg = (N + nthr - 1) / nthr;
   const int q0 = min(N, tid * seg), q1 = min(N, q0 + seg);
-  unsigned lsum = 0, lpairs = 0;
+  unsigned lsum = 0;
   constexpr int US = 16;
   // the root (q = 0) pairs with every pixel; the commit kernel fills its row
   // with a grid-wide row scan, so its chunks are left out of the partition
@@ -856,10 +876,8 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
 #pragma unroll
     for (int j = 0; j < US; j++) {
       lsum += (qb + j) ? ((unsigned)x[j] + 31u) >> 5 : 0u;
-      lpairs += x[j];
     }
   }
-  atomicAdd(&sh.pairs, lpairs);
   unsigned incl = lsum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -902,7 +920,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
     unsigned b = (unsigned)((double)num / (double)P);  // floor(p*T/P), exact fix-up
     while ((unsigned long long)b * P > num) b--;
     while ((unsigned long long)(b + 1) * P <= num) b++;
-    gpart[pp] = (uint32_t)q | ((b - runq) << 16);
+    __stcs(&gpart[pp], (uint32_t)q | ((b - runq) << 16));
   };
   // positions owning many units (near the root) are queued and written by
   // whole warps; the rest by their thread
@@ -950,6 +968,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
     __syncthreads();
     if (tid == 0) dbg[5] = gtimer();
   }
+  }  // !lite
   if (a.publish) {  // the tree is complete: make it visible to the commit loop
     __threadfence();
     __syncthreads();
