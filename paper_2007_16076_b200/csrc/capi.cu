@@ -184,7 +184,7 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
 extern "C" int gp_ctx_num_pixels(const gp_ctx* c) { return c ? c->g.N : 0; }
 
 enum { WS_SEQ, WS_NEW, WS_SRC, WS_SLOT_OF, WS_RANK, WS_EXT, WS_SELKEY, WS_FLAGS, WS_CTL, WS_DFC,
-       WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK, WS_EXTK, WS_EXTT };
+       WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK, WS_EXTK, WS_EXTT, WS_CSET };
 
 template <typename T>
 static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
@@ -806,6 +806,12 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     CommitArgs ca;
     memset(&ca, 0, sizeof(ca));
     ca.fillq = getenv("GP_FILL_QUEUE") ? atoi(getenv("GP_FILL_QUEUE")) != 0 : 1;
+    // candidate-set selection (k_commit fast path); GP_CAND=0 off
+    if (!getenv("GP_CAND") || atoi(getenv("GP_CAND")) != 0) {
+      uint32_t* d_cset = nullptr;
+      CUDA_TRY(ws_get(c, WS_CSET, &d_cset, 1024));
+      ca.cand = d_cset;
+    }
     ca.g = c->g;
     ca.L = L;
     ca.strategy = strategy == GP_STRATEGY_FILLING_RATE ? kFillingRate : kNaive;

@@ -92,6 +92,14 @@ __device__ __forceinline__ unsigned long long sel_pack(unsigned key, int v, int 
          (unsigned long long)(slot >= 0 && slot < 0xFFFF ? (unsigned)(slot + 1) : 0u);
 }
 
+// Candidate set (filling-rate): while selecting, the open pixels with key < T
+// are also collected into cand[] (CAND_CAP at most).  Keys only grow, so at a
+// later step every pixel outside the set still has key >= T; if the least
+// current key inside the set is below T it is the global minimum, and every
+// CTA can compute it redundantly from the set -- no grid-wide argmin and no
+// second grid barrier for that step (k_commit fast path).
+constexpr int CAND_CAP = 1024;
+
 __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned long long* red64) {
   const int N = a.g.N;
   unsigned long long m = ~0ull;
@@ -106,6 +114,32 @@ __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned lo
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nopen += __shfl_xor_sync(0xffffffffu, nopen, o);
     if ((threadIdx.x & 31) == 0 && nopen) atomicAdd(&a.dbgo[step], (unsigned long long)nopen);
+  }
+  m = block_reduce_min(m, red64);
+  if (threadIdx.x == 0 && m != ~0ull) atomicMin(&a.selkey[step], m);
+}
+
+// the same selection, also collecting the candidate set (keys below candT)
+__device__ void select_collect(const CommitArgs& a, int step, int skip, unsigned long long* red64,
+                               unsigned candT) {
+  const int N = a.g.N;
+  unsigned long long m = ~0ull;
+  for (int v0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); v0 < N; v0 += gridDim.x * blockDim.x) {
+    const int v = v0 + (threadIdx.x & 31);
+    unsigned key = 0xFFFFFFFFu;
+    if (v < N && v != skip) {
+      key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
+      if (key != 0xFFFFFFFFu) m = min(m, sel_pack(key, v, __ldcg(&a.slot_of[v])));
+    }
+    const bool in = key < candT;  // warp-aggregated append of the keys below the threshold
+    const unsigned bm = __ballot_sync(0xffffffffu, in);
+    if (bm) {
+      unsigned base = 0;
+      if ((threadIdx.x & 31) == 0) base = atomicAdd(&a.ctl->cand_cnt[step & 1], (unsigned)__popc(bm));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const unsigned pos = base + __popc(bm & ((1u << (threadIdx.x & 31)) - 1u));
+      if (in && pos < (unsigned)CAND_CAP) a.cand[pos] = (uint32_t)v | ((key & 0xFFFFu) << 16);
+    }
   }
   m = block_reduce_min(m, red64);
   if (threadIdx.x == 0 && m != ~0ull) atomicMin(&a.selkey[step], m);
@@ -681,9 +715,18 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   __shared__ unsigned long long red64[32];
   __shared__ int unit_ctr[2];  // per-CTA work-unit counters (alternating steps)
   __shared__ FillQ fq;         // per-CTA chunk queue (tree mode)
+  __shared__ uint32_t cand_s[CAND_CAP];  // candidate set: pixel | rank << 16
+  __shared__ unsigned long long sel_s;   // fast-path selection broadcast
+  // candidate-set state, CTA-uniform (shared memory, not registers)
+  __shared__ unsigned cand_n, cand_T, cand_delta, cur_key;
+  const bool use_cand = a.cand != nullptr && a.strategy == kFillingRate;
   if (threadIdx.x == 0) {
     unit_ctr[0] = unit_ctr[1] = 0;
     fq.n = fq.res = fq.head = 0;
+    cand_delta = use_cand ? max(1u, __ldcg(&a.ctl->cand_delta)) : 0u;
+    cand_n = 0;  // valid set: 0 < cand_n <= CAND_CAP (a previous launch's set is not reused)
+    cand_T = 0;
+    cur_key = 0;  // selection key of the current source
   }
   __syncthreads();
   if (a.ctl->status == CTL_DONE) return;  // pipelined loop: launched past the end
@@ -705,6 +748,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     visits = a.ctl->visits;
     dead = a.ctl->list_dead;
   }
+  if (keeper && use_cand) a.ctl->cand_cnt[0] = a.ctl->cand_cnt[1] = 0;  // visible after the first barrier
   int slot = -1;
   if (s == -1) {  // first launch: select the first source
     select_step(a, step, -1, red64);
@@ -713,6 +757,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   if (s != -2) {  // (re)load the packed selection of `step`
     const unsigned long long sk = __ldcg(&a.selkey[step]);
     s = sk == ~0ull ? -2 : (int)((sk >> 16) & 0xFFFFu);
+    if (threadIdx.x == 0) cur_key = (unsigned)(sk >> 32);
     if (s >= 0) slot = __ldcg(&a.slot_of[s]);  // may have been propagated since
   }
   int status = CTL_RUNNING;
@@ -787,11 +832,49 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
       a.cnt[s] = N - 1;  // the root pairs with every pixel
       a.seq[step] = s;
       a.slot_of[s] = -2;  // committed
+      // collection counter of the next step's selection (this step's selection
+      // uses the other one; the last reads of this one preceded this barrier)
+      if (use_cand) a.ctl->cand_cnt[step & 1] = 0;
     }
     // ---- K3: selection of the next source (+ keeper's accounting) ----
     unsigned long long stepnew = 0;
     if (keeper) stepnew = __ldcg(&a.newp[step]);  // in flight with the selection loads
-    select_step(a, step + 1, s, red64);
+    // Fast path (candidate set valid): the least current key among the
+    // candidates, if below T, is the global minimum; every CTA derives it, so
+    // the step needs no grid-wide argmin and no second grid barrier.  The
+    // step's flags (list switch, compaction) are left for the next slow step:
+    // both are performance decisions only.
+    bool fast = false;
+    unsigned long long sk = ~0ull;
+    if (use_cand && !compact && cand_n) {
+      unsigned long long m = ~0ull;
+      for (unsigned i = threadIdx.x; i < cand_n; i += blockDim.x) {
+        const uint32_t e = cand_s[i];
+        const int v = (int)(e & 0xFFFFu);
+        if (v == s) continue;
+        const int c = __ldcg(&a.cnt[v]);
+        const int sl = __ldcg(&a.slot_of[v]);
+        if (c < N - 1) m = min(m, sel_pack(((unsigned)c << 16) | (e >> 16), v, sl));
+      }
+      m = block_reduce_min(m, red64);
+      if (threadIdx.x == 0) sel_s = m;
+      __syncthreads();
+      m = sel_s;
+      fast = m != ~0ull && (unsigned)(m >> 32) < cand_T;
+      __syncthreads();  // every thread has read cand_n / cand_T / sel_s
+      if (fast) {
+        sk = m;
+        if (keeper) a.selkey[step + 1] = m;
+      } else if (threadIdx.x == 0) {
+        cand_n = 0;  // exhausted: this step's grid-wide selection rebuilds it
+      }
+    }
+    unsigned candT_new = 0;
+    if (!fast) {
+      if (use_cand && !compact) candT_new = (((cur_key >> 16) + cand_delta) << 16);
+      if (candT_new) select_collect(a, step + 1, s, red64, candT_new);
+      else select_step(a, step + 1, s, red64);
+    }
     if (keeper) {
       filled += stepnew;
       visits += cslot;
@@ -803,17 +886,34 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
       a.stepflags[step + 1] = f;
     }
     if (dbg) dbg[3] = gtimer();
-    grid_barrier(a.bar, gen);
-    const unsigned long long sk = __ldcg(&a.selkey[step + 1]);
-    flags = __ldcg(&a.stepflags[step + 1]);
-    if (compact) {  // swap buffers; the new length is final after the barrier
-      if (keeper) a.ctl->list_n[lcur] = 0;
-      lcur ^= 1u;
-      ln = __ldcg(&a.ctl->list_n[lcur]);
+    if (fast) {
+      flags = 0;
+    } else {
+      grid_barrier(a.bar, gen);
+      sk = __ldcg(&a.selkey[step + 1]);
+      flags = __ldcg(&a.stepflags[step + 1]);
+      if (compact) {  // swap buffers; the new length is final after the barrier
+        if (keeper) a.ctl->list_n[lcur] = 0;
+        lcur ^= 1u;
+        ln = __ldcg(&a.ctl->list_n[lcur]);
+      }
+      if (candT_new) {  // the set collected with the selection (ordered before the
+                        // next fast path by the fill's block reductions)
+        const unsigned n = __ldcg(&a.ctl->cand_cnt[(step + 1) & 1]);
+        const unsigned nv = (n > 0 && n <= (unsigned)CAND_CAP) ? n : 0u;
+        for (unsigned i = threadIdx.x; i < nv; i += blockDim.x) cand_s[i] = __ldcg(&a.cand[i]);
+        if (threadIdx.x == 0) {
+          cand_n = nv;
+          cand_T = candT_new;
+          if (n > (unsigned)CAND_CAP) cand_delta = max(1u, cand_delta >> 1);
+          else if (n < (unsigned)CAND_CAP / 8) cand_delta = min(cand_delta << 1, 4096u);
+        }
+      }
     }
     step++;
     done_here++;
     s = sk == ~0ull ? -2 : (int)((sk >> 16) & 0xFFFFu);
+    if (threadIdx.x == 0) cur_key = (unsigned)(sk >> 32);
     slot = (int)(sk & 0xFFFFu) - 1;
     if (slot < 0 && s >= 0) slot = __ldcg(&a.slot_of[s]);  // not encodable / no tree yet
     if (flags & 1u) { status = CTL_SWITCH; break; }
@@ -826,6 +926,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     a.ctl->visits = visits;
     a.ctl->list_dead = dead;
     a.ctl->list_cur = lcur;
+    if (use_cand) a.ctl->cand_delta = cand_delta;
   }
 }
 

@@ -76,7 +76,9 @@ struct Ctl {
   unsigned list_dead;         // dead entries in the live buffer
   unsigned long long list_switch;  // switch to list mode when unfilled <= this
   int build;                       // list build pending (set by k_switch_prep)
-  int pad3;
+  unsigned cand_delta;             // candidate-set width in counts (k_commit, adaptive)
+  unsigned cand_cnt[2];            // candidate collection counters (step parity)
+  unsigned pad4;
 };
 enum { CTL_RUNNING = 0, CTL_DONE = 1, CTL_MISS = 2, CTL_LIMIT = 3, CTL_SWITCH = 4 };
 
@@ -115,6 +117,7 @@ struct CommitArgs {
   unsigned long long* dbgo; // optional per-step open-pixel counts (debug dump)
   GridBarrier* bar;
   uint32_t* plist[2];      // unfilled pairs (u << 16 | w, u < w), list mode
+  uint32_t* cand;          // [CAND_CAP] candidate set (pixel | rank << 16); nullptr: off
   unsigned long long total_pairs;
 };
 
