@@ -29,7 +29,7 @@ def main():
         if len(r) != len(hdr):
             continue
         name = r[K].split("(")[0].replace("void ", "").strip()
-        name = name.split("<")[0]
+        name = name.split("<")[0].split("::")[-1]
         k = acc.setdefault(name, {"launches": set(), "dram_bytes": 0.0, "ms": 0.0})
         k["launches"].add(r[I])
         val = float(r[V].replace(",", "")) * UNIT.get(r[U], 1.0)
