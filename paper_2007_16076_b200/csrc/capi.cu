@@ -946,7 +946,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
           EvPair e;
           cudaEventCreate(&e.a); cudaEventCreate(&e.b);
           CUDA_TRY(cudaEventRecord(e.a, st));
-          CUDA_TRY(launch_commit(ca, nblocks, st));
+          CUDA_TRY(commit_split() ? launch_commit_split(ca, nblocks, st) : launch_commit(ca, nblocks, st));
           CUDA_TRY(cudaEventRecord(e.b, st));
           cev.push_back(e);
           S.launches++;
@@ -974,7 +974,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       EvPair e;
       cudaEventCreate(&e.a); cudaEventCreate(&e.b);
       CUDA_TRY(cudaEventRecord(e.a, st));
-      CUDA_TRY(launch_commit(ca, nblocks, st));
+      CUDA_TRY(commit_split() ? launch_commit_split(ca, nblocks, st) : launch_commit(ca, nblocks, st));
       CUDA_TRY(cudaEventRecord(e.b, st));
       CUDA_TRY(cudaEventRecord(ev_c, st));
       cev.push_back(e);

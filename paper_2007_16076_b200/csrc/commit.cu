@@ -710,7 +710,11 @@ __device__ __forceinline__ void compact_list(const CommitArgs& a, unsigned cur, 
   }
 }
 
-template <int G, int THREADS, int MINB>
+// MODE: -1 = the run's mode read at launch; 0 / 1 = tree / list mode only
+// (the launch returns at once in the other mode).  A mode-specific kernel
+// keeps the other mode's code out of its register allocation, and the list
+// kernel runs twice the threads per SM.
+template <int G, int THREADS, int MINB, int MODE = -1>
 __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   __shared__ unsigned long long red64[32];
   __shared__ int unit_ctr[2];  // per-CTA work-unit counters (alternating steps)
@@ -730,6 +734,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   }
   __syncthreads();
   if (a.ctl->status == CTL_DONE) return;  // pipelined loop: launched past the end
+  if (MODE >= 0 && a.ctl->mode != MODE) return;  // the other mode's kernel runs
   const int N = a.g.N;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const bool keeper = gtid == 0;  // bookkeeping thread (registers, stores only)
@@ -737,7 +742,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
 
   int step = a.ctl->step;
   int s = a.ctl->cur_src;
-  const int mode = a.ctl->mode;
+  const int mode = MODE >= 0 ? MODE : a.ctl->mode;
   // launch-invariant / register-resident state
   unsigned lcur = mode ? __ldcg(&a.ctl->list_cur) : 0u;
   unsigned ln = mode ? __ldcg(&a.ctl->list_n[lcur]) : 0u;
@@ -977,6 +982,51 @@ cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st) 
   void* params[] = {&args};
   return cudaLaunchCooperativeKernel(commit_kernel(commit_fill_depth()), dim3(num_blocks),
                                      dim3(commit_threads()), params, 0, st);
+}
+
+// Mode-split commit loop (1024-thread configuration): the tree-mode kernel
+// (one 1024-thread CTA per SM) and the list-mode kernel (LIST_THREADS x
+// LIST_MINB per SM) are both enqueued; the one not matching the run's mode
+// returns at once.
+// list kernel shape: GP_LIST_CFG = 0 (1024 x 1 per SM), 1 (1024 x 2), 2 (512 x 2)
+static int list_cfg() {
+  static int v = -1;
+  if (v < 0) v = getenv("GP_LIST_CFG") ? atoi(getenv("GP_LIST_CFG")) : 0;
+  return v;
+}
+
+static const void* list_kernel() {
+  return list_cfg() == 1 ? (const void*)k_commit<4, 1024, 2, 1>
+       : list_cfg() == 2 ? (const void*)k_commit<4, 512, 2, 1> : (const void*)k_commit<4, 1024, 1, 1>;
+}
+
+static int list_threads() { return list_cfg() == 2 ? 512 : 1024; }
+
+static int list_blocks() {
+  static int nb = 0;
+  if (!nb) {
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, list_kernel(), list_threads(), 0);
+    nb = nsm * std::max(1, std::min(per_sm, list_cfg() == 0 ? 1 : 2));
+  }
+  return nb;
+}
+
+bool commit_split() {
+  static int v = -1;
+  if (v < 0) v = getenv("GP_COMMIT_SPLIT") ? (atoi(getenv("GP_COMMIT_SPLIT")) != 0) : 1;
+  return v != 0 && commit_threads() == 1024;
+}
+
+cudaError_t launch_commit_split(const CommitArgs& a, int num_blocks, cudaStream_t st) {
+  CommitArgs args = a;
+  void* params[] = {&args};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_commit<4, 1024, 1, 0>, dim3(num_blocks),
+                                              dim3(1024), params, 0, st);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchCooperativeKernel(list_kernel(), dim3(list_blocks()), dim3(list_threads()), params, 0, st);
 }
 
 // ---- list-mode entry: every unfilled pair (u < w) from the mark bitmap ----

@@ -125,6 +125,8 @@ void commit_configure(int N);
 int commit_threads();
 constexpr uint32_t LIST_DEAD = 0xFFFFFFFFu;
 cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st);
+bool commit_split();
+cudaError_t launch_commit_split(const CommitArgs& a, int num_blocks, cudaStream_t st);
 int commit_max_blocks();
 int commit_fill_depth();
 cudaError_t launch_topk(const CommitArgs& a, int K, int Q, int* cands, int* slots,
