@@ -735,6 +735,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   __syncthreads();
   if (a.ctl->status == CTL_DONE) return;  // pipelined loop: launched past the end
   if (MODE >= 0 && a.ctl->mode != MODE) return;  // the other mode's kernel runs
+  // the mode-specific kernels are also lean: no debug instrumentation and the
+  // chunk-queue tree fill only (commit_split() sends other runs to MODE -1)
+  constexpr bool LEAN = MODE >= 0;
   const int N = a.g.N;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const bool keeper = gtid == 0;  // bookkeeping thread (registers, stores only)
@@ -772,15 +775,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     if (s == -2) { status = CTL_DONE; break; }
     if (done_here >= a.max_steps) { status = CTL_LIMIT; break; }
     if (slot < 0) { status = CTL_MISS; break; }
-    unsigned long long* dbg = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + (size_t)step * 4 : nullptr;
+    unsigned long long* dbg = (!LEAN && a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + (size_t)step * 4 : nullptr;
     if (dbg) dbg[0] = gtimer();
-    const unsigned long long tw0 = a.dbgw ? gtimer() : 0ull;
+    const unsigned long long tw0 = (!LEAN && a.dbgw) ? gtimer() : 0ull;
     const unsigned cslot = keeper ? __ldg(&a.ts.C[slot]) : 0u;  // consumed at step end
     // ---- K2: fill ----
     unsigned long long lnew = 0;
     if (mode == 1) {
-      lnew = fill_list(a, slot, s, lcur, ln, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr);
-    } else if (a.fillq) {
+      lnew = fill_list(a, slot, s, lcur, ln, (!LEAN && a.dbgs) ? a.dbgs + (size_t)step * 8 : nullptr);
+    } else if (LEAN || a.fillq) {
       lnew = fill_tree_cta<G>(a, slot, s, fq, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr);
     } else {
       // Work units of this tree are interleaved over the CTAs (unit = b + k *
@@ -816,14 +819,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     }
     if (mode == 0) lnew += fill_root_row(a, slot, s);
     if (dbg) dbg[1] = gtimer();
-    if (a.dbgw && (threadIdx.x & 31) == 0) {
+    if (!LEAN && a.dbgw && (threadIdx.x & 31) == 0) {
       const unsigned long long dt = gtimer() - tw0;
       atomicMax(&a.dbgw[(size_t)step * 4], dt);
       atomicAdd(&a.dbgw[(size_t)step * 4 + 1], dt);
     }
     lnew = block_reduce_sum(lnew, red64);
     if (threadIdx.x == 0) fq.n = fq.res = fq.head = 0;  // all warps are past the fill
-    if (a.dbgw && threadIdx.x == 0) {
+    if (!LEAN && a.dbgw && threadIdx.x == 0) {
       const unsigned long long dt = gtimer() - tw0;
       atomicMax(&a.dbgw[(size_t)step * 4 + 2], dt);
       atomicAdd(&a.dbgw[(size_t)step * 4 + 3], dt);
@@ -995,36 +998,46 @@ static int list_cfg() {
   return v;
 }
 
+// (the 512-thread configuration of smaller maps keeps 512 x 2 for both modes)
 static const void* list_kernel() {
+  if (commit_threads() != 1024) return (const void*)k_commit<4, 512, 2, 1>;
   return list_cfg() == 1 ? (const void*)k_commit<4, 1024, 2, 1>
        : list_cfg() == 2 ? (const void*)k_commit<4, 512, 2, 1> : (const void*)k_commit<4, 1024, 1, 1>;
 }
 
-static int list_threads() { return list_cfg() == 2 ? 512 : 1024; }
+static int list_threads() { return (commit_threads() != 1024 || list_cfg() == 2) ? 512 : 1024; }
 
 static int list_blocks() {
-  static int nb = 0;
-  if (!nb) {
+  static int nb[2] = {0, 0};  // per commit configuration (512 / 1024 threads)
+  const int k = commit_threads() == 1024 ? 1 : 0;
+  if (!nb[k]) {
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, list_kernel(), list_threads(), 0);
-    nb = nsm * std::max(1, std::min(per_sm, list_cfg() == 0 ? 1 : 2));
+    nb[k] = nsm * std::max(1, std::min(per_sm, (k && list_cfg() == 0) ? 1 : 2));
   }
-  return nb;
+  return nb[k];
 }
 
 bool commit_split() {
   static int v = -1;
-  if (v < 0) v = getenv("GP_COMMIT_SPLIT") ? (atoi(getenv("GP_COMMIT_SPLIT")) != 0) : 1;
-  return v != 0 && commit_threads() == 1024;
+  if (v < 0) {
+    v = getenv("GP_COMMIT_SPLIT") ? (atoi(getenv("GP_COMMIT_SPLIT")) != 0) : 1;
+    // the split kernels carry no debug instrumentation and only the queue fill
+    if ((getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"))) ||
+        (getenv("GP_FILL_QUEUE") && !atoi(getenv("GP_FILL_QUEUE"))))
+      v = 0;
+  }
+  return v != 0 && (commit_threads() == 1024 || commit_fill_depth() == 4);
 }
 
 cudaError_t launch_commit_split(const CommitArgs& a, int num_blocks, cudaStream_t st) {
   CommitArgs args = a;
   void* params[] = {&args};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_commit<4, 1024, 1, 0>, dim3(num_blocks),
-                                              dim3(1024), params, 0, st);
+  const void* tk = commit_threads() == 1024 ? (const void*)k_commit<4, 1024, 1, 0>
+                                            : (const void*)k_commit<4, 512, 2, 0>;
+  cudaError_t e = cudaLaunchCooperativeKernel(tk, dim3(num_blocks), dim3(commit_threads()), params, 0, st);
   if (e != cudaSuccess) return e;
   return cudaLaunchCooperativeKernel(list_kernel(), dim3(list_blocks()), dim3(list_threads()), params, 0, st);
 }
