@@ -35,6 +35,7 @@
 // of it runs here, off the commit loop's critical path.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "gp_common.cuh"
 #include "gp_kernels.h"
@@ -180,8 +181,14 @@ __device__ void pointer_jump_global(uint32_t* pj, int N) {
   }
 }
 
-template <int THR, int MINB>
+// VAR: 0 = generic (variant, outputs and debug stamps decided at run time);
+// 1 / 2 = lean global-scratch / shared-memory variant for speculative
+// batches: Euler-tour outputs only, no naive epilogue, no API outputs, no
+// debug stamps -- each gets its own register allocation.
+template <int THR, int MINB, int VAR = 0>
 __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
+  constexpr bool LEAN = VAR != 0;
+  const bool in_smem = VAR == 2 ? true : VAR == 1 ? false : a.in_smem != 0;
   const Grid g = a.g;
   const int N = g.N, NW = (N + 31) >> 5;
   const int t = blockIdx.x;
@@ -189,12 +196,12 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   const int lane = tid & 31, wid = tid >> 5;
   if (a.ntrees_dev && t >= *a.ntrees_dev) return;
   __shared__ PropShared sh;
-  unsigned long long* dbg = a.dbg ? a.dbg + (size_t)t * 16 : nullptr;
+  unsigned long long* dbg = (!LEAN && a.dbg) ? a.dbg + (size_t)t * 16 : nullptr;
   if (dbg && tid == 0) { dbg[0] = gtimer(); dbg[12] = 0; dbg[13] = 0; }
 
-  const size_t hist_cap = a.in_smem ? HIST_SMEM : HIST_G;
+  const size_t hist_cap = in_smem ? HIST_SMEM : HIST_G;
   const Layout lay = prop_layout(N, hist_cap);
-  unsigned char* base = a.in_smem ? g_smem : a.scratch + (size_t)t * a.scratch_bytes;
+  unsigned char* base = in_smem ? g_smem : a.scratch + (size_t)t * a.scratch_bytes;
   uint32_t* dist = reinterpret_cast<uint32_t*>(base);
   float* fimg = reinterpret_cast<float*>(base + lay.A);
   WorkLists wl;
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   uint32_t* far = reinterpret_cast<uint32_t*>(base + lay.far);
   uint32_t* inq = reinterpret_cast<uint32_t*>(base + lay.inq);
   uint32_t* hist = reinterpret_cast<uint32_t*>(base + lay.hist);
-  if (a.in_smem) {
+  if (in_smem) {
     wl.s[0] = wl.g[0];
     wl.s[1] = wl.g[1];
     wl.cap = N;
@@ -221,8 +228,8 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
     code = g_smem + 2 * bm;
     hist = reinterpret_cast<uint32_t*>(g_smem + 2 * bm + align16((size_t)(N + 1) / 2));
   }
-  const float* f = a.in_smem ? fimg : a.img;
-  if (a.in_smem)
+  const float* f = in_smem ? fimg : a.img;
+  if (in_smem)
     for (int i = tid; i < N; i += nthr) fimg[i] = a.img[i];
   // volatile: in the global-scratch variant, plain loads could hit a stale L1
   // line after atomics performed at L2.
@@ -267,7 +274,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
             if (b) {
               const int bit = __ffs(b) - 1;
               b &= b - 1;
-              dd[j] = a.in_smem ? vdist[(w << 5) + bit] : __ldcg(&dist[(w << 5) + bit]);
+              dd[j] = in_smem ? vdist[(w << 5) + bit] : __ldcg(&dist[(w << 5) + bit]);
             }
           }
 #pragma unroll
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
             if (b) {
               bb[j] = __ffs(b) - 1;
               b &= b - 1;
-              dd[j] = a.in_smem ? vdist[(w << 5) + bb[j]] : __ldcg(&dist[(w << 5) + bb[j]]);
+              dd[j] = in_smem ? vdist[(w << 5) + bb[j]] : __ldcg(&dist[(w << 5) + bb[j]]);
             }
           }
 #pragma unroll
@@ -341,7 +348,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
     }
     if (tid == 0) sh.cnt[cur ^ 1] = 0;
     __syncthreads();
-    if (!a.in_smem) {
+    if (!in_smem) {
       // global variant: RR rounds of (item, edge) pairs per thread in flight
       // together -- distance loads, then independent atomics at L2.  The
       // worklist is read from shared memory directly while it fits there; the
@@ -432,7 +439,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
             const uint32_t nb = __float_as_uint(nd);
             // pre-check (cheap in smem); in the global variant the atomic's
             // returned value is the check, saving a dependent L2 round trip
-            if (!a.in_smem || nb < vdist[u]) {
+            if (!in_smem || nb < vdist[u]) {
               const uint32_t old = atomicMin(&dist[u], nb);
               if (nb < old) {
                 const uint32_t ub = 1u << (u & 31);
@@ -476,7 +483,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       cbyte |= 15u << (4 * h);
       continue;
     }
-    const uint32_t dvb = a.in_smem ? vdist[v] : __ldcg(&dist[v]);
+    const uint32_t dvb = in_smem ? vdist[v] : __ldcg(&dist[v]);
     if (!((vfar[v >> 5] >> (v & 31)) & 1u)) {
       const float dv = __uint_as_float(dvb);
       int r, c;
@@ -491,7 +498,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
         if (!k_in_conn(g.conn, k)) continue;
         const int u = nbr_at(g, r, c, k);
         if (u < 0) continue;
-        dub[k] = a.in_smem ? vdist[u] : __ldcg(&dist[u]);
+        dub[k] = in_smem ? vdist[u] : __ldcg(&dist[u]);
         fu[k] = f[u];
       }
       uint32_t best = INF_BITS;
@@ -508,7 +515,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       if (cv == GP_ROOT) unparented = 1;
     }
     cbyte |= (cv == GP_ROOT ? 15u : (unsigned)cv) << (4 * h);
-    if (a.out_dist) a.out_dist[off + v] = __uint_as_float(dvb);
+    if (!LEAN && a.out_dist) a.out_dist[off + v] = __uint_as_float(dvb);
    }
    code[pp] = (uint8_t)cbyte;
   }
@@ -569,11 +576,11 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
     for (int i = tid; i < NW; i += nthr) inq[i] = 0;
     __syncthreads();
   }
-  if (a.out_dir)
+  if (!LEAN && a.out_dir)
     for (int v = tid; v < N; v += nthr) a.out_dir[off + v] = code_get(vcode, v);
 
   // ---------------- naive epilogue: fill_from_source, row/column x > s ----
-  if (a.D) {
+  if (!LEAN && a.D) {
     const int s = my_src[0];
     float* D = a.D;
     for (int x = s + 1 + tid; x < N; x += nthr) {
@@ -593,13 +600,13 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
     pj[v] = cv == GP_ROOT ? (uint32_t)v : ((1u << 16) | (uint32_t)parent_of(v, cv, g.W));
   }
   __syncthreads();
-  if (a.in_smem) pointer_jump(pj, N);
+  if (in_smem) pointer_jump(pj, N);
   else pointer_jump_global(const_cast<uint32_t*>(pj), N);
   if (dbg && tid == 0) dbg[3] = gtimer();
   // Loops over arrays that are stable within a phase read them from L2 in the
   // global variant (__ldcg: no stale L1) and directly in shared memory; UB
   // iterations' loads are issued before any is consumed.
-  const bool gm = !a.in_smem;
+  const bool gm = !in_smem;
   auto rd32 = [gm](const volatile uint32_t* p) -> uint32_t {
     return gm ? __ldcg(const_cast<const uint32_t*>(p)) : *p;
   };
@@ -679,7 +686,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   // E4: descendant counts, deepest level first -- one warp, no block barriers
   // (shared-memory variant); block-wide per level in the global variant,
   // where one warp would pay a global round trip per level and element
-  if (use_hist && !a.in_smem) {
+  if (use_hist && !in_smem) {
     // the first entry of the next level is loaded before this level's barrier
     int vn = -1;
     if (maxd >= 1 && vhist[maxd - 1] + tid < vhist[maxd]) vn = order[vhist[maxd - 1] + tid];
@@ -775,7 +782,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   }
   __syncthreads();
   if (dbg && tid == 0) dbg[14] = gtimer();
-  if (a.in_smem) pointer_jump(pj, N);
+  if (in_smem) pointer_jump(pj, N);
   else pointer_jump_global(const_cast<uint32_t*>(pj), N);
   if (dbg && tid == 0) dbg[4] = gtimer();
   // Tree-store outputs are written with evict-first stores (st.global.cs): the
@@ -1004,12 +1011,15 @@ static int prop_threads(int N) {
   return threads;
 }
 
-static const void* prop_kernel(int N, int threads) {
+static const void* prop_kernel(const PropArgs& a, int N, int threads) {
   const size_t per_cta = prop_dyn_smem(N) + 1024 + sizeof(PropShared);
   int minb = 3;
   if (const char* e = getenv("GP_PROP_MINB")) minb = atoi(e);
+  const bool lean = !a.dbg && !a.D && !a.out_dist && !a.out_dir && a.ts.pre &&
+                    !(getenv("GP_PROP_LEAN") && !atoi(getenv("GP_PROP_LEAN")));
   if (!prop_fits_smem(N) && threads == 512 && minb == 3 && (228 * 1024) / per_cta >= 3)
-    return (const void*)k_propagate<512, 3>;
+    return lean ? (const void*)k_propagate<512, 3, 1> : (const void*)k_propagate<512, 3>;
+  if (lean) return prop_fits_smem(N) ? (const void*)k_propagate<1024, 1, 2> : (const void*)k_propagate<1024, 1, 1>;
   return (const void*)k_propagate<1024, 1>;
 }
 
@@ -1018,7 +1028,10 @@ static const void* prop_kernel(int N, int threads) {
 int prop_trees_per_sm(int N) {
   if (prop_fits_smem(N)) return 2;
   const int threads = prop_threads(N);
-  const void* k = prop_kernel(N, threads);
+  PropArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  pa.ts.pre = reinterpret_cast<uint32_t*>(1);  // a speculative batch: lean when allowed
+  const void* k = prop_kernel(pa, N, threads);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prop_dyn_smem(N));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, prop_dyn_smem(N));
@@ -1031,7 +1044,7 @@ cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st) {
   if (!a.in_smem) a.scratch_bytes = prop_scratch_bytes(a.g.N);
   const size_t smem = prop_dyn_smem(a.g.N);
   const int threads = a.threads ? a.threads : prop_threads(a.g.N);
-  const void* kern = prop_kernel(a.g.N, threads);
+  const void* kern = prop_kernel(a, a.g.N, threads);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   void* params[] = {&a};
