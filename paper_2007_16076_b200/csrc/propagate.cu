@@ -185,11 +185,14 @@ __device__ void pointer_jump_global(uint32_t* pj, int N) {
 // 1 / 2 = lean global-scratch / shared-memory variant for speculative
 // batches: Euler-tour outputs only, no naive epilogue, no API outputs, no
 // debug stamps -- each gets its own register allocation.
-template <int THR, int MINB, int VAR = 0>
+// MC = 1: SUM metric and 8-connectivity fixed at compile time (the BASELINE
+// configurations but config 3); 0: read from the grid.
+template <int THR, int MINB, int VAR = 0, int MC = 0>
 __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   constexpr bool LEAN = VAR != 0;
   const bool in_smem = VAR == 2 ? true : VAR == 1 ? false : a.in_smem != 0;
   const Grid g = a.g;
+  const int gmetric = MC ? (int)kSum : g.metric, gconn = MC ? 8 : g.conn;
   const int N = g.N, NW = (N + 31) >> 5;
   const int t = blockIdx.x;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
             const int v = wl_fits ? (int)lsm[it] : (int)*wl.at(cur, it);
             int k = idx & 7;
             k += (k >= 4);
-            if (k_in_conn(g.conn, k)) {
+            if (k_in_conn(gconn, k)) {
               int r, c;
               pix_rc(g, v, r, c);
               const int dr = (int)((0x2A540u >> (2 * k)) & 3u) - 1;  // k / 3 - 1
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
               if ((unsigned)(r + dr) < (unsigned)g.H && (unsigned)(c + dc) < (unsigned)g.W) {
                 uk[j] = v + dr * g.W + dc;
                 dvk[j] = __ldcg(&dist[v]);
-                fwk[j] = edge_w(g.metric, __ldg(&f[v]), __ldg(&f[uk[j]]));
+                fwk[j] = edge_w(gmetric, __ldg(&f[v]), __ldg(&f[uk[j]]));
               }
             }
           }
@@ -430,12 +433,12 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
         const int v = *wl.at(cur, idx >> 3);
         int k = idx & 7;
         k += (k >= 4);
-        if (k_in_conn(g.conn, k)) {
+        if (k_in_conn(gconn, k)) {
           int r, c;
           pix_rc(g, v, r, c);
           u = nbr_at(g, r, c, k);
           if (u >= 0) {
-            const float nd = __fadd_rn(__uint_as_float(vdist[v]), edge_w(g.metric, f[v], f[u]));
+            const float nd = __fadd_rn(__uint_as_float(vdist[v]), edge_w(gmetric, f[v], f[u]));
             const uint32_t nb = __float_as_uint(nd);
             // pre-check (cheap in smem); in the global variant the atomic's
             // returned value is the check, saving a dependent L2 round trip
@@ -495,7 +498,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       for (int k = 0; k < 9; k++) {  // all neighbour loads in flight together
         dub[k] = INF_BITS;
         fu[k] = 0.0f;
-        if (!k_in_conn(g.conn, k)) continue;
+        if (!k_in_conn(gconn, k)) continue;
         const int u = nbr_at(g, r, c, k);
         if (u < 0) continue;
         dub[k] = in_smem ? vdist[u] : __ldcg(&dist[u]);
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       for (int k = 0; k < 9; k++) {
         if (dub[k] == INF_BITS) continue;
         const int u = v + (k / 3 - 1) * g.W + (k % 3 - 1);
-        const float cand = __fadd_rn(__uint_as_float(dub[k]), edge_w(g.metric, fu[k], fv));
+        const float cand = __fadd_rn(__uint_as_float(dub[k]), edge_w(gmetric, fu[k], fv));
         if (cand == dv && (dub[k] < dvb || (dub[k] == dvb && u < v)) && dub[k] < best) {
           best = dub[k];
           cv = (uint8_t)k;
@@ -556,10 +559,10 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
         pix_rc(g, v, r, c);
         const float dv = __uint_as_float(vdist[v]);
         for (int k = 0; k < 9; k++) {
-          if (!k_in_conn(g.conn, k)) continue;
+          if (!k_in_conn(gconn, k)) continue;
           const int u = nbr_at(g, r, c, k);
           if (u < 0 || !((vcon[u >> 5] >> (u & 31)) & 1u)) continue;
-          if (__fadd_rn(__uint_as_float(vdist[u]), edge_w(g.metric, f[u], f[v])) != dv) continue;
+          if (__fadd_rn(__uint_as_float(vdist[u]), edge_w(gmetric, f[u], f[v])) != dv) continue;
           code_set(vcode, v, (unsigned)k);
           atomicOr(&far[v >> 5], 1u << (v & 31));
           changed = 1;
@@ -756,7 +759,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       const bool interior = pr > 0 && pr < g.H - 1 && pc > 0 && pc < g.W - 1;
 #pragma unroll
       for (int k = 0; k < 9; k++) {
-        if (!k_in_conn(g.conn, k)) continue;
+        if (!k_in_conn(gconn, k)) continue;
         if (!interior && nbr_at(g, pr, pc, k) < 0) continue;
         if (code_get(vcode, pp + (k / 3 - 1) * g.W + (k % 3 - 1)) == (uint8_t)(8 - k)) mask[b] |= 1u << k;
       }
@@ -1017,9 +1020,15 @@ static const void* prop_kernel(const PropArgs& a, int N, int threads) {
   if (const char* e = getenv("GP_PROP_MINB")) minb = atoi(e);
   const bool lean = !a.dbg && !a.D && !a.out_dist && !a.out_dir && a.ts.pre &&
                     !(getenv("GP_PROP_LEAN") && !atoi(getenv("GP_PROP_LEAN")));
-  if (!prop_fits_smem(N) && threads == 512 && minb == 3 && (228 * 1024) / per_cta >= 3)
-    return lean ? (const void*)k_propagate<512, 3, 1> : (const void*)k_propagate<512, 3>;
-  if (lean) return prop_fits_smem(N) ? (const void*)k_propagate<1024, 1, 2> : (const void*)k_propagate<1024, 1, 1>;
+  const bool mc = a.g.metric == kSum && a.g.conn == 8 && !(getenv("GP_PROP_MC") && !atoi(getenv("GP_PROP_MC")));
+  if (!prop_fits_smem(N) && threads == 512 && minb == 3 && (228 * 1024) / per_cta >= 3) {
+    if (lean) return mc ? (const void*)k_propagate<512, 3, 1, 1> : (const void*)k_propagate<512, 3, 1>;
+    return (const void*)k_propagate<512, 3>;
+  }
+  if (lean) {
+    if (prop_fits_smem(N)) return mc ? (const void*)k_propagate<1024, 1, 2, 1> : (const void*)k_propagate<1024, 1, 2>;
+    return (const void*)k_propagate<1024, 1, 1>;
+  }
   return (const void*)k_propagate<1024, 1>;
 }
 
