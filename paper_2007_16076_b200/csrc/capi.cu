@@ -806,6 +806,8 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     CommitArgs ca;
     memset(&ca, 0, sizeof(ca));
     ca.fillq = getenv("GP_FILL_QUEUE") ? atoi(getenv("GP_FILL_QUEUE")) != 0 : 1;
+    ca.compact_div = 4;
+    if (const char* e = getenv("GP_COMPACT_DIV")) ca.compact_div = (unsigned)std::max(1, atoi(e));
     // candidate-set selection (k_commit fast path); GP_CAND=0 off
     if (!getenv("GP_CAND") || atoi(getenv("GP_CAND")) != 0) {
       uint32_t* d_cset = nullptr;

@@ -890,7 +890,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
       const unsigned live = compact ? 0u : ln;  // new length unknown yet: no back-to-back compaction
       unsigned f = 0;
       if (mode == 0 && a.total_pairs - filled <= a.ctl->list_switch) f |= 1u;
-      if (mode == 1 && live && (unsigned long long)dead * 4 > live) f |= 2u;
+      if (mode == 1 && live && (unsigned long long)dead * a.compact_div > live) f |= 2u;
       a.stepflags[step + 1] = f;
     }
     if (dbg) dbg[3] = gtimer();
