@@ -52,6 +52,8 @@ struct gp_ctx {
   int commit_blocks = 0;
   double mean_w = 1.0;  // mean edge weight (bucket width scale)
   uint32_t* list[2] = {nullptr, nullptr};  // unfilled-pair lists (late phase)
+  int* h_cnt2 = nullptr;     // pinned: two count snapshots (host-row rounds)
+  Ctl* h_ctl2 = nullptr;     // pinned: two control-block snapshots
   void* ws[32] = {};      // run workspace, cached across runs (no cudaMalloc in gp_run)
   size_t ws_bytes[32] = {};
   size_t list_cap = 0;
@@ -178,6 +180,8 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
   if (c->st2) cudaStreamDestroy(c->st2);
   if (c->st3) cudaStreamDestroy(c->st3);
   if (c->h_cnt) cudaFreeHost(c->h_cnt);
+  if (c->h_cnt2) cudaFreeHost(c->h_cnt2);
+  if (c->h_ctl2) cudaFreeHost(c->h_ctl2);
   delete c;
 }
 
@@ -578,6 +582,7 @@ struct RowStreamer {
   float* host;
   std::vector<uint8_t> sent;
   int64_t rows_sent = 0;
+  int open_rows = -1;  // rows not complete at the last snapshot
   cudaEvent_t snap_ev = nullptr;
   bool snap_pending = false;
   // counts snapshot in stream order (the caller enqueues it at a quiescent
@@ -599,18 +604,24 @@ struct RowStreamer {
   ~RowStreamer() {
     if (snap_ev) cudaEventDestroy(snap_ev);
   }
-  int enqueue(bool all, bool read = true) {
+  int enqueue(bool all, bool read = true, const int* cnt = nullptr) {
     const int N = c->g.N;
     if (!host) return GP_OK;
     if (!all && read) {
       CUDA_TRY(cudaMemcpyAsync(c->h_cnt, s->cnt, (size_t)N * 4, cudaMemcpyDeviceToHost, c->st));
       CUDA_TRY(cudaStreamSynchronize(c->st));
     }
+    const int* hc = cnt ? cnt : c->h_cnt;
+    if (!all) {
+      int open = 0;
+      for (int v = 0; v < N; v++) open += hc[v] != N - 1;
+      open_rows = open;
+    }
     int u = 0;
     while (u < N) {
-      if (sent[u] || (!all && c->h_cnt[u] != N - 1)) { u++; continue; }
+      if (sent[u] || (!all && hc[u] != N - 1)) { u++; continue; }
       int e = u;
-      while (e < N && !sent[e] && (all || c->h_cnt[e] == N - 1)) sent[e++] = 1;
+      while (e < N && !sent[e] && (all || hc[e] == N - 1)) sent[e++] = 1;
       CUDA_TRY(cudaMemcpyAsync(host + (size_t)u * N, s->D + (size_t)u * N, (size_t)(e - u) * N * 4,
                                cudaMemcpyDeviceToHost, c->st3));
       rows_sent += e - u;
@@ -927,7 +938,9 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       }
       ca.plist[0] = c->list[0];
       ca.plist[1] = c->list[1];
-      constexpr int CHUNK = 6;
+      // rounds per host check; with host rows, single rounds once few rows
+      // are open, so the rows still to copy after the last commit are few
+      const int chunk = 6;
       auto prop_batch = [&](int gated) -> int {
         EvPair f;
         cudaEventCreate(&f.a); cudaEventCreate(&f.b);
@@ -939,12 +952,67 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
         S.kernels += 2;
         return GP_OK;
       };
+      auto round = [&]() -> int {  // one round: commit launch(es), batch, list switch
+        EvPair e;
+        cudaEventCreate(&e.a); cudaEventCreate(&e.b);
+        CUDA_TRY(cudaEventRecord(e.a, st));
+        CUDA_TRY(commit_split() ? launch_commit_split(ca, nblocks, st) : launch_commit(ca, nblocks, st));
+        CUDA_TRY(cudaEventRecord(e.b, st));
+        cev.push_back(e);
+        S.launches++;
+        S.kernels++;
+        if (int r = prop_batch(1)) return r;
+        CUDA_TRY(launch_switch(ca, c->list[0], st));
+        S.kernels += 2;
+        return GP_OK;
+      };
       hmark("ctx/args");
       if (int r = prop_batch(0)) return r;
       hmark("first batch enqueued");
-      for (int guard = 0; guard < 8 * N + 16; guard += CHUNK) {
+      if (D_host) {
+        // Host rows: rounds with one round of lookahead.  Each round ends with
+        // copies of the counts and the control block into pinned buffers
+        // (alternating); while round r runs, the host reads round r-1's
+        // status and queues the D rows it completed on the copy stream, so
+        // the GPU never waits for the host (rows left after the last commit:
+        // ~400, 4 ms of D2H, against ~40 ms with the 6-round host checks).
+        int e2e_cap = 0;  // GP_E2E_CAP: cap commit launches once half the rows are complete (0: off)
+        if (const char* e = getenv("GP_E2E_CAP")) e2e_cap = atoi(e);
+        if (!c->h_cnt2) CUDA_TRY(cudaHostAlloc(&c->h_cnt2, (size_t)2 * N * 4, cudaHostAllocDefault));
+        if (!c->h_ctl2) CUDA_TRY(cudaHostAlloc(&c->h_ctl2, 2 * sizeof(Ctl), cudaHostAllocDefault));
+        cudaEvent_t rev[2];
+        cudaEventCreateWithFlags(&rev[0], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&rev[1], cudaEventDisableTiming);
+        auto end_round = [&](int b) -> int {
+          CUDA_TRY(cudaMemcpyAsync(c->h_cnt2 + (size_t)b * N, s->cnt, (size_t)N * 4, cudaMemcpyDeviceToHost, st));
+          CUDA_TRY(cudaMemcpyAsync(c->h_ctl2 + b, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+          CUDA_TRY(cudaEventRecord(rev[b], st));
+          return GP_OK;
+        };
+        if (int r = round()) return r;
+        if (int r = end_round(0)) return r;
+        for (int rr = 1; rr < 8 * N + 16; rr++) {
+          if (int r = round()) return r;
+          if (int r = end_round(rr & 1)) return r;
+          const int b = (rr - 1) & 1;
+          CUDA_TRY(cudaEventSynchronize(rev[b]));  // round rr-1 done, round rr running
+          const Ctl hc = c->h_ctl2[b];
+          if (hc.status == CTL_DONE) break;
+          if (hc.status == CTL_LIMIT && ca.max_steps > N) {
+            rc = fail(GP_EINTERNAL, "commit loop stopped unexpectedly");
+            break;
+          }
+          if (int r = rs.enqueue(false, false, c->h_cnt2 + (size_t)b * N)) return r;
+          if (rs.open_rows >= 0 && rs.open_rows < N / 2 && e2e_cap > 0) ca.max_steps = e2e_cap;
+        }
+        CUDA_TRY(cudaStreamSynchronize(st));
+        cudaEventDestroy(rev[0]);
+        cudaEventDestroy(rev[1]);
+        CUDA_TRY(cudaMemcpy(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+      }
+      for (int guard = 0; !D_host && guard < 8 * N + 16; guard += chunk) {
         if (guard) rs.snapshot();  // quiescent point: the previous chunk is complete
-        for (int it = 0; it < CHUNK; it++) {
+        for (int it = 0; it < chunk; it++) {
           EvPair e;
           cudaEventCreate(&e.a); cudaEventCreate(&e.b);
           CUDA_TRY(cudaEventRecord(e.a, st));
@@ -961,7 +1029,10 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
         CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
         if (h_ctl.status == CTL_DONE) break;
-        if (h_ctl.status == CTL_LIMIT) { rc = fail(GP_EINTERNAL, "commit loop stopped unexpectedly"); break; }
+        if (h_ctl.status == CTL_LIMIT && ca.max_steps > N) {
+          rc = fail(GP_EINTERNAL, "commit loop stopped unexpectedly");
+          break;
+        }
       }
       S.batches = h_ctl.batches;
     }
@@ -1094,8 +1165,15 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   }
   if (D_host && !rc) {
     CUDA_TRY(cudaStreamSynchronize(st));
+    hmark("run done (device)");
+    const int64_t before = rs.rows_sent;
+    CUDA_TRY(cudaStreamSynchronize(c->st3));
+    hmark("streamed copies drained");
     if (int r = rs.enqueue(true)) return r;
     CUDA_TRY(cudaStreamSynchronize(c->st3));
+    hmark("final rows copied");
+    if (htime) fprintf(stderr, "[gp host] rows streamed during the run %lld, after %lld (open at last snapshot %d)\n",
+                       (long long)before, (long long)(rs.rows_sent - before), rs.open_rows);
   }
   S.ms_total = ev_ms(tot);
   S.ms_setup = ev_ms(setup);
