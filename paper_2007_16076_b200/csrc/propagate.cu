@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       // worklist is read from shared memory directly while it fits there; the
       // window offsets come from packed constants, one unsigned compare per
       // bound; the appends of the RR rounds share one counter update.
-      constexpr int RR = 4;
+      constexpr int RR = 2;  // measured: 1 -> 615, 2 -> 600, 3 -> 609, 4 -> 614, 6 -> 659 ms per 256^2 image
       const int items = n * 8;
       const bool wl_fits = n <= wl.cap;
       const uint16_t* lsm = wl.s[cur];
