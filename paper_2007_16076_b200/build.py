@@ -36,7 +36,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if not force and not needs_build():
         return OUT
     srcs = [os.path.join(HERE, "csrc", s) for s in SOURCES]
-    cmd = [NVCC, *FLAGS, "-o", OUT, *srcs]
+    extra = os.environ.get("GP_NVCC_EXTRA", "").split()  # dev: tuning -D flags
+    cmd = [NVCC, *FLAGS, *extra, "-o", OUT, *srcs]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -624,7 +624,10 @@ __device__ __forceinline__ void grid_barrier(GridBarrier* bar, unsigned& gen) {
 // ends of a pair cost one gather each).  Work per commit = unfilled pairs
 // (shrinking), instead of the tree's ~N*depth pairs; LU entries per thread
 // are in flight together.
-constexpr int LU = 4;
+#ifndef GP_LU
+#define GP_LU 4
+#endif
+constexpr int LU = GP_LU;
 __device__ __forceinline__ unsigned fill_list(const CommitArgs& a, int slot, int s,
                                               unsigned cur, unsigned n,
                                               unsigned long long* prb = nullptr) {

@@ -44,6 +44,17 @@ namespace gp {
 
 extern __shared__ __align__(16) unsigned char g_smem[];
 
+// loads in flight per thread in the global-scratch loops (tuned on B200)
+#ifndef GP_PJ_CHAINS
+#define GP_PJ_CHAINS 4
+#endif
+#ifndef GP_UB
+#define GP_UB 8
+#endif
+#ifndef GP_UE
+#define GP_UE 4
+#endif
+
 constexpr int HIST_SMEM = 4096;  // depth-histogram bins in the shared-memory variant
 constexpr int HIST_G = 1024;     // depth-histogram bins in smem (global-scratch variant)
 constexpr int WL_SMEM = 9216;    // worklist entries kept in smem (global-scratch variant)
@@ -155,20 +166,20 @@ __device__ void pointer_jump(volatile uint32_t* pj, int N) {
 __device__ void pointer_jump_global(uint32_t* pj, int N) {
   for (;;) {
     int ch = 0;
-    for (int v0 = threadIdx.x; v0 < N; v0 += 4 * blockDim.x) {
-      uint32_t pr[4], px[4];
+    for (int v0 = threadIdx.x; v0 < N; v0 += GP_PJ_CHAINS * blockDim.x) {
+      uint32_t pr[GP_PJ_CHAINS], px[GP_PJ_CHAINS];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
+      for (int j = 0; j < GP_PJ_CHAINS; j++) {
         const int v = v0 + j * blockDim.x;
         pr[j] = v < N ? __ldcg(&pj[v]) : 0u;
       }
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
+      for (int j = 0; j < GP_PJ_CHAINS; j++) {
         const int v = v0 + j * blockDim.x;
         px[j] = v < N ? __ldcg(&pj[pr[j] & 0xFFFFu]) : 0u;
       }
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
+      for (int j = 0; j < GP_PJ_CHAINS; j++) {
         const int v = v0 + j * blockDim.x;
         const uint32_t jj = px[j] & 0xFFFFu;
         if (v < N && jj != (pr[j] & 0xFFFFu)) {
@@ -616,7 +627,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   auto rd16 = [gm](const volatile uint16_t* p) -> uint16_t {
     return gm ? __ldcg(const_cast<const unsigned short*>(p)) : *p;
   };
-  constexpr int UB = 8;
+  constexpr int UB = GP_UB;
   // E2: depth (B) and max depth
   volatile uint16_t* depth = reinterpret_cast<volatile uint16_t*>(base + lay.B);
   // C = ancestor/descendant pairs of the tree = sum of depths
@@ -798,7 +809,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   // reads them from L2 (__ldcg: no stale L1, loads pipeline), smem directly.
   float* gtdp = a.ts.tdp + off;
   uint32_t* gtin = a.ts.tin + off;
-  constexpr int UE = 4;
+  constexpr int UE = GP_UE;
   for (int v0 = tid; v0 < N; v0 += UE * nthr) {
     uint32_t x[UE], dv[UE];
     uint16_t sz[UE];
