@@ -98,7 +98,10 @@ __device__ __forceinline__ unsigned long long sel_pack(unsigned key, int v, int 
 // current key inside the set is below T it is the global minimum, and every
 // CTA can compute it redundantly from the set -- no grid-wide argmin and no
 // second grid barrier for that step (k_commit fast path).
-constexpr int CAND_CAP = 1024;
+#ifndef GP_CAND_CAP
+#define GP_CAND_CAP 1024
+#endif
+constexpr int CAND_CAP = GP_CAND_CAP;
 
 __device__ void select_step(const CommitArgs& a, int step, int skip, unsigned long long* red64) {
   const int N = a.g.N;
@@ -294,7 +297,10 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
 // fill_unit (deep trees).  Descriptor: x = pre entry of the ancestor u
 // (tile column << 16 | u); y = qb | chunk << 16 | (valid lanes - 1) << 27,
 // qb = preorder position of u's first descendant.
-constexpr int FQ_CAP = 4096;
+#ifndef GP_FQ_CAP
+#define GP_FQ_CAP 4096
+#endif
+constexpr int FQ_CAP = GP_FQ_CAP;
 struct FillQ {
   uint2 desc[FQ_CAP];
   int n, res, head;
