@@ -101,6 +101,12 @@ __device__ __forceinline__ uint8_t code_get(const volatile uint8_t* code, int v)
   return c == 15u ? GP_ROOT : (uint8_t)c;
 }
 
+// set the code of a root pixel (nibble 15) to k: one atomic
+__device__ __forceinline__ void code_set_root(uint8_t* code, int v, unsigned k) {
+  unsigned* w = reinterpret_cast<unsigned*>(code) + (v >> 3);
+  atomicAnd(w, ~((15u ^ k) << ((v & 7) << 2)));
+}
+
 // set the code of pixel v to k (the other nibbles of the word may change
 // concurrently: both steps are atomic)
 __device__ __forceinline__ void code_set(volatile uint8_t* code, int v, unsigned k) {
@@ -486,17 +492,16 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   const size_t off = (size_t)slot * N;
   volatile uint8_t* vcode = code;
   int unparented = 0;
-  // one thread per pixel pair: the two 4-bit codes of a byte are stored together
-  for (int pp = tid; 2 * pp < N; pp += nthr) {
-   unsigned cbyte = 0;
-#pragma unroll 1
-   for (int h = 0; h < 2; h++) {
-    const int v = 2 * pp + h;
+  // one thread per pixel: the code array starts all roots (nibbles 15) and a
+  // parented pixel clears its nibble down to k with one shared atomic (the
+  // neighbouring pixel of the same byte may be written concurrently)
+  {
+    uint32_t* cw = reinterpret_cast<uint32_t*>(code);
+    for (int i = tid; i < (N + 7) / 8; i += nthr) cw[i] = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  for (int v = tid; v < N; v += nthr) {
     uint8_t cv = GP_ROOT;
-    if (v >= N) {
-      cbyte |= 15u << (4 * h);
-      continue;
-    }
     const uint32_t dvb = in_smem ? vdist[v] : __ldcg(&dist[v]);
     if (!((vfar[v >> 5] >> (v & 31)) & 1u)) {
       const float dv = __uint_as_float(dvb);
@@ -528,10 +533,8 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       }
       if (cv == GP_ROOT) unparented = 1;
     }
-    cbyte |= (cv == GP_ROOT ? 15u : (unsigned)cv) << (4 * h);
+    if (cv != GP_ROOT) code_set_root(code, v, cv);
     if (!LEAN && a.out_dist) a.out_dist[off + v] = __uint_as_float(dvb);
-   }
-   code[pp] = (uint8_t)cbyte;
   }
   // Zero-weight plateaus (L1 metric only).  A pixel without a tight neighbour
   // of smaller (d, id) is a local root, and pixels parented so far may hang
