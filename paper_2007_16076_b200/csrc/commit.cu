@@ -672,11 +672,12 @@ __device__ __forceinline__ unsigned fill_list(const CommitArgs& a, int slot, int
     for (int j = 0; j < LU; j++) {
       if (e[j] == LIST_DEAD) continue;
       const unsigned tu = zu[j] & 0xFFFFu, tw = zw[j] & 0xFFFFu;
-      int anc, des;
-      unsigned ta, td;
-      if (tu < tw && tw <= tu + (zu[j] >> 16)) { anc = (int)(e[j] >> 16); des = (int)(e[j] & 0xFFFFu); ta = tu; td = tw; }
-      else if (tw < tu && tu <= tw + (zw[j] >> 16)) { anc = (int)(e[j] & 0xFFFFu); des = (int)(e[j] >> 16); ta = tw; td = tu; }
-      else continue;
+      // u ancestor of w iff 0 < tw - tu <= size(u): one unsigned compare each way
+      const bool uw = tw - tu - 1u < (zu[j] >> 16), wu = tu - tw - 1u < (zw[j] >> 16);
+      if (!(uw | wu)) continue;
+      const int anc = uw ? (int)(e[j] >> 16) : (int)(e[j] & 0xFFFFu);
+      const int des = uw ? (int)(e[j] & 0xFFFFu) : (int)(e[j] >> 16);
+      const unsigned ta = uw ? tu : tw, td = uw ? tw : tu;
       const uint32_t ca = mcol(L, (uint32_t)anc), cd = mcol(L, (uint32_t)des);
       atomicOr(&a.mark[mword(L, (uint32_t)anc, cd)], 1u << (cd & 31));
       atomicOr(&a.mark[mword(L, (uint32_t)des, ca)], 1u << (ca & 31));
