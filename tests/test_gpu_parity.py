@@ -123,6 +123,12 @@ def test_config_matches_golden(gp, index):
     assert np.allclose(rows, g["row_sum"], rtol=1e-9, atol=0)
     if spec.n <= 16384:
         assert _digest(Dd.cpu().numpy(), isf) == str(g["d_sha256"])
+    else:  # 16 GiB at 256x256: hashed in row blocks (the same bytes in the same order)
+        h = hashlib.sha256()
+        for r0 in range(0, spec.n, 2048):
+            blk = Dd[r0:r0 + 2048].cpu().numpy()
+            h.update(np.ascontiguousarray(blk).astype("<f4" if isf else "<i4").tobytes())
+        assert h.hexdigest() == str(g["d_sha256"])
 
 
 def test_api_known_answers(gp):
