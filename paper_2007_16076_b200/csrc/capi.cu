@@ -737,7 +737,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     commit_configure(overlap ? 0 : N);
     const int nblocks = commit_blocks(c, overlap);
     hmark("commit_blocks");
-    int uf = N >= 32768 ? 4 : 1;  // work units per commit warp (dynamic balancing)
+    int uf = N >= 32768 ? 3 : 1;  // work units per commit warp (measured at 256^2: 2 933, 3 915, 4 917, 8 1011 ms)
     if (const char* e = getenv("GP_UNITS_PER_WARP")) uf = std::max(1, atoi(e));
     const int nparts = nblocks * (commit_threads() / 32) * uf;
     int rts = ensure_tree_store(c, nparts);
