@@ -1235,6 +1235,32 @@ __global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int Q, int* 
     }
   }
   __syncthreads();
+  if (a.lpt) {
+    // Longest trees first: a batch runs in one or more waves of CTAs in
+    // blockIdx order, and a tree's time grows with its depth (relaxation
+    // passes >= depth), which the source's eccentricity bounds from below
+    // (Chebyshev distance to the farthest corner for 8-connectivity,
+    // Manhattan for 4).  Candidates sorted by it, deepest first, so the
+    // shallow trees of a batch fill the slots the first wave frees.
+    __shared__ unsigned long long lk[1024];
+    const int n = min(s_n, K);
+    const Grid g = a.g;
+    for (int i = tid; i < n; i += blockDim.x) {
+      const int v = cands[i];
+      const int r = v / g.W, c = v - r * g.W;
+      const int dr = max(r, g.H - 1 - r), dc = max(c, g.W - 1 - c);
+      const unsigned ecc = g.conn == 8 ? (unsigned)max(dr, dc) : (unsigned)(dr + dc);
+      lk[i] = ((unsigned long long)(0xFFFFu - ecc) << 32) | (unsigned)v;  // ascending = deepest first
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) {
+      const unsigned long long me = lk[i];
+      int rk = 0;
+      for (int j = 0; j < n; j++) rk += lk[j] < me;
+      cands[rk] = (int)(me & 0xFFFFFFFFu);
+    }
+    __syncthreads();
+  }
   if (tid == 0) {
     const int n = min(s_n, K);
     Ctl* c = a.ctl;

@@ -119,6 +119,7 @@ struct CommitArgs {
   uint32_t* plist[2];      // unfilled pairs (u << 16 | w, u < w), list mode
   uint32_t* cand;          // [CAND_CAP] candidate set (pixel | rank << 16); nullptr: off
   unsigned compact_div;    // list mode: compact when dead entries > live / compact_div
+  int lpt;                 // top-K: candidates deepest-first (longest trees first in the batch)
   unsigned long long total_pairs;
 };
 

@@ -89,7 +89,7 @@ def test_l1_plateau_run_completes_with_exact_distances(gp, oracle, shape):
     {"GP_UNITS_PER_WARP": "4"}, {"GP_DELTA_FACTOR": "inf"}, {"GP_DELTA_FACTOR": "0.5"},
     {"GP_PROP_THREADS": "256"}, {"GP_BARRIER": "sw"}, {"GP_PIPELINE": "0"}, {"GP_FILL_QUEUE": "0"},
     {"GP_FILL_UNROLL": "1"}, {"GP_FILL_UNROLL": "8"}, {"GP_OVERLAP": "1"}, {"GP_PROP_MINB": "2"},
-    {"GP_CAND": "0"}, {"GP_COMMIT_SPLIT": "0"}, {"GP_LIST_CFG": "2"}, {"GP_PROP_LEAN": "0"}, {"GP_PROP_MC": "0"},
+    {"GP_CAND": "0"}, {"GP_LPT": "0"}, {"GP_COMMIT_SPLIT": "0"}, {"GP_LIST_CFG": "2"}, {"GP_PROP_LEAN": "0"}, {"GP_PROP_MC": "0"},
 ])
 def test_tuning_knobs_do_not_change_results(gp, oracle, env, monkeypatch):
     img = np.random.default_rng(11).random((24, 20), dtype=np.float32)
