@@ -6,6 +6,7 @@ import os
 
 import numpy as np
 import pytest
+import torch
 
 pytestmark = pytest.mark.gpu
 
@@ -231,3 +232,31 @@ def test_global_scratch_propagation_matches_oracle(gp, oracle, shape, conn, metr
             assert np.array_equal(r.parent, p), s
         else:
             _check_tree(np.asarray(r.dist, dtype=np.float32), r.parent, img, conn, metric, [s])
+
+
+@pytest.mark.parametrize("shape,conn,isint", [((64, 1024), 8, True), ((256, 256), 4, False)])
+def test_max_size_runs_rows_equal_propagations(gp, oracle, shape, conn, isint):
+    """Maximum-size maps (65 536 pixels; a non-square one and a 4-connected
+    fp32 one -- shapes no BASELINE config uses): the completed array is
+    symmetric with a zero diagonal, every count is N-1, and row s equals the
+    oracle's propagation from s (D[s][x] = geodesic distance s -> x): exactly
+    for integer images; for fp32 images within rounding, since an entry holds
+    the difference of two distances of the tree that filled it."""
+    rng = np.random.default_rng(sum(shape) + conn)
+    img = rng.integers(1, 256, shape) if isint else rng.random(shape, dtype=np.float32)
+    run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, gp.StrategyKind.FILLING_RATE,
+                          connectivity=conn, force=True)
+    N = shape[0] * shape[1]
+    assert run.distances.is_complete
+    assert np.array_equal(run.distances.point_filled_counts, np.full(N, N - 1))
+    Dd = run.distances.dist_device()
+    assert bool((torch.diagonal(Dd) == 0).all())
+    for r0 in range(0, N, 8192):  # symmetry in row blocks (16 GiB array)
+        assert bool((Dd[r0:r0 + 8192] == Dd[:, r0:r0 + 8192].T).all())
+    for s in [0, N - 1] + [int(x) for x in rng.choice(N, 3, replace=False)]:
+        d, _ = oracle.propagate(img, [s], conn=conn)
+        row = Dd[s].cpu().numpy()
+        if isint:
+            assert np.array_equal(row, np.asarray(d, dtype=np.float32)), s
+        else:
+            assert np.allclose(row, d, rtol=1e-4, atol=1e-6), s
