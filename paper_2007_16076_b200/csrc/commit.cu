@@ -972,12 +972,10 @@ static const void* commit_kernel(int G) {
        : G == 1 ? (const void*)k_commit<1, 512, 2> : (const void*)k_commit<2, 512, 2>;
 }
 
+// (knobs are read at every call, so a process can switch them between runs)
 int commit_fill_depth() {
-  static int g = 0;
-  if (!g) {
-    g = 4;
-    if (const char* e = getenv("GP_FILL_UNROLL")) g = atoi(e) >= 8 ? 8 : atoi(e) >= 4 ? 4 : atoi(e) == 1 ? 1 : 2;
-  }
+  int g = 4;
+  if (const char* e = getenv("GP_FILL_UNROLL")) g = atoi(e) >= 8 ? 8 : atoi(e) >= 4 ? 4 : atoi(e) == 1 ? 1 : 2;
   return g;
 }
 
@@ -1003,9 +1001,8 @@ cudaError_t launch_commit(const CommitArgs& a, int num_blocks, cudaStream_t st) 
 // returns at once.
 // list kernel shape: GP_LIST_CFG = 0 (1024 x 1 per SM), 1 (1024 x 2), 2 (512 x 2)
 static int list_cfg() {
-  static int v = -1;
-  if (v < 0) v = getenv("GP_LIST_CFG") ? atoi(getenv("GP_LIST_CFG")) : 0;
-  return v;
+  const int v = getenv("GP_LIST_CFG") ? atoi(getenv("GP_LIST_CFG")) : 0;
+  return v >= 0 && v <= 2 ? v : 0;
 }
 
 // (the 512-thread configuration of smaller maps keeps 512 x 2 for both modes)
@@ -1018,27 +1015,25 @@ static const void* list_kernel() {
 static int list_threads() { return (commit_threads() != 1024 || list_cfg() == 2) ? 512 : 1024; }
 
 static int list_blocks() {
-  static int nb[2] = {0, 0};  // per commit configuration (512 / 1024 threads)
-  const int k = commit_threads() == 1024 ? 1 : 0;
-  if (!nb[k]) {
+  static int nb[2][3] = {};  // per commit configuration (512 / 1024 threads) and list shape
+  const int k = commit_threads() == 1024 ? 1 : 0, lc = list_cfg();
+  int* cached = &nb[k][lc];
+  if (!*cached) {
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, list_kernel(), list_threads(), 0);
-    nb[k] = nsm * std::max(1, std::min(per_sm, (k && list_cfg() == 0) ? 1 : 2));
+    *cached = nsm * std::max(1, std::min(per_sm, (k && lc == 0) ? 1 : 2));
   }
-  return nb[k];
+  return *cached;
 }
 
 bool commit_split() {
-  static int v = -1;
-  if (v < 0) {
-    v = getenv("GP_COMMIT_SPLIT") ? (atoi(getenv("GP_COMMIT_SPLIT")) != 0) : 1;
-    // the split kernels carry no debug instrumentation and only the queue fill
-    if ((getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"))) ||
-        (getenv("GP_FILL_QUEUE") && !atoi(getenv("GP_FILL_QUEUE"))))
-      v = 0;
-  }
+  int v = getenv("GP_COMMIT_SPLIT") ? (atoi(getenv("GP_COMMIT_SPLIT")) != 0) : 1;
+  // the split kernels carry no debug instrumentation and only the queue fill
+  if ((getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"))) ||
+      (getenv("GP_FILL_QUEUE") && !atoi(getenv("GP_FILL_QUEUE"))))
+    v = 0;
   return v != 0 && (commit_threads() == 1024 || commit_fill_depth() == 4);
 }
 
