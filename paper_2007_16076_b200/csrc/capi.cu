@@ -567,6 +567,7 @@ static int store_relayout(gp_store* s, const MarkLayout& L) {
 static int commit_blocks(gp_ctx* c, bool overlap) {
   const int maxb = commit_max_blocks();
   int bps = overlap ? 1 : 2048 / commit_threads();
+  if (c->g.N < 16384) bps = 1;  // tiny fills: the barrier over fewer CTAs wins (64^2: 26.9 -> 25.0 ms)
   if (const char* e = getenv("GP_COMMIT_BLOCKS_PER_SM")) bps = atoi(e);
   return std::max(1, std::min(maxb, bps * c->nsm));
 }
