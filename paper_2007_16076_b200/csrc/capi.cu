@@ -778,7 +778,9 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     // late phase: switch to the unfilled-pair list when the unfilled pairs drop
     // below alpha x the pairs of one tree (~N * mean depth); GP_LIST_ALPHA=0 off
     {
-      double alpha = N >= 32768 ? 1.0 : 3.0;  // measured: 256^2 flat in [1, 1.5]; 128^2 and 64^2 best at 3
+      // measured: 256^2 flat in [1, 1.5]; 128^2 best at 3-5; 64^2 at 10
+      // (1 for tiny test images, which then exercise the tree fill too)
+      double alpha = N >= 32768 ? 1.0 : N > 8192 ? 3.0 : N > 1024 ? 10.0 : 1.0;
       if (const char* e = getenv("GP_LIST_ALPHA")) alpha = atof(e);
       const double est_tree = (double)N * std::sqrt((double)N) * 0.5;
       double sw = alpha * est_tree;
