@@ -99,7 +99,7 @@ __device__ __forceinline__ unsigned long long sel_pack(unsigned key, int v, int 
 // CTA can compute it redundantly from the set -- no grid-wide argmin and no
 // second grid barrier for that step (k_commit fast path).
 #ifndef GP_CAND_CAP
-#define GP_CAND_CAP 1024
+#define GP_CAND_CAP 512  // measured: 384 911, 512 910, 640 912, 1024 915 ms (256^2); 128^2 118 vs 122.5 at 1024
 #endif
 constexpr int CAND_CAP = GP_CAND_CAP;
 
