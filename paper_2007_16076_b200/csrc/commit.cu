@@ -98,6 +98,9 @@ __device__ __forceinline__ unsigned long long sel_pack(unsigned key, int v, int 
 // current key inside the set is below T it is the global minimum, and every
 // CTA can compute it redundantly from the set -- no grid-wide argmin and no
 // second grid barrier for that step (k_commit fast path).
+#ifndef GP_CAND_GROW
+#define GP_CAND_GROW 8  // widen the candidate window while the set holds < CAP / GROW
+#endif
 #ifndef GP_CAND_CAP
 #define GP_CAND_CAP 512  // measured: 384 911, 512 910, 640 912, 1024 915 ms (256^2); 128^2 118 vs 122.5 at 1024
 #endif
@@ -924,7 +927,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
           cand_n = nv;
           cand_T = candT_new;
           if (n > (unsigned)CAND_CAP) cand_delta = max(1u, cand_delta >> 1);
-          else if (n < (unsigned)CAND_CAP / 8) cand_delta = min(cand_delta << 1, 4096u);
+          else if (n < (unsigned)CAND_CAP / GP_CAND_GROW) cand_delta = min(cand_delta << 1, 4096u);
         }
       }
     }
