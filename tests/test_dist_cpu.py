@@ -54,3 +54,15 @@ def test_aggregation_single_rank():
 
     total_ms, value = bench.aggregate(500.0, 10, 5, 1)
     assert total_ms == 500.0 and value == pytest.approx(100.0)
+
+
+def test_committed_traffic_evidence_feeds_roofline():
+    """bench.py's roofline.traffic comes from the committed ncu capture of the
+    headline config; the commit kernels' bytes must be present and consistent."""
+    import bench
+
+    k, src = bench._traffic(5, "k_commit")
+    assert src is not None and src.startswith("profiles/")
+    assert k["launches"] > 0 and k["dram_bytes"] > 0
+    assert abs(k["dram_bytes_per_launch"] * k["launches"] - k["dram_bytes"]) < 1e-6 * k["dram_bytes"]
+    assert bench._traffic(999, "k_commit") == (None, None)
