@@ -90,7 +90,8 @@ def test_l1_plateau_run_completes_with_exact_distances(gp, oracle, shape):
     {"GP_UNITS_PER_WARP": "4"}, {"GP_DELTA_FACTOR": "inf"}, {"GP_DELTA_FACTOR": "0.5"},
     {"GP_PROP_THREADS": "256"}, {"GP_BARRIER": "sw"}, {"GP_PIPELINE": "0"}, {"GP_FILL_QUEUE": "0"},
     {"GP_FILL_UNROLL": "1"}, {"GP_FILL_UNROLL": "8"}, {"GP_OVERLAP": "1"}, {"GP_PROP_MINB": "2"},
-    {"GP_CAND": "0"}, {"GP_LPT": "0"}, {"GP_COMMIT_SPLIT": "0"}, {"GP_LIST_CFG": "2"}, {"GP_PROP_LEAN": "0"}, {"GP_PROP_MC": "0"},
+    {"GP_CAND": "0"}, {"GP_LPT": "0"}, {"GP_COMMIT_SPLIT": "0"}, {"GP_LIST_CFG": "2"}, {"GP_LIST_CFG": "1"}, {"GP_PROP_LEAN": "0"}, {"GP_PROP_MC": "0"},
+    {"GP_COMPACT_DIV": "1"}, {"GP_COMPACT_DIV": "64"}, {"GP_LIST_ALPHA": "1", "GP_COMPACT_DIV": "1"},
 ])
 def test_tuning_knobs_do_not_change_results(gp, oracle, env, monkeypatch):
     img = np.random.default_rng(11).random((24, 20), dtype=np.float32)
@@ -125,10 +126,15 @@ def test_metric_properties_of_completed_array(gp):
     assert int((D[x, z] > D[x, y] + D[y, z]).sum()) == 0
 
 
-@pytest.mark.parametrize("shape,kind", [((40, 37), 1), ((64, 64), 1), ((23, 30), 0)])
-def test_run_to_host_streams_the_same_array(gp, shape, kind):
-    """gp_run_to_host (rows streamed during the run) == gp_run + gp_store_read."""
+@pytest.mark.parametrize("shape,kind,cap", [((40, 37), 1, 0), ((64, 64), 1, 0), ((23, 30), 0, 0),
+                                            ((64, 64), 1, 3)])
+def test_run_to_host_streams_the_same_array(gp, shape, kind, cap, monkeypatch):
+    """gp_run_to_host (rows streamed during the run) == gp_run + gp_store_read;
+    cap > 0: GP_E2E_CAP (short commit launches once half the rows are done)."""
     import ctypes
+
+    if cap:
+        monkeypatch.setenv("GP_E2E_CAP", str(cap))
 
     import torch
 
