@@ -72,6 +72,8 @@ typedef struct {
   double ms_propagate;     /* device time inside propagation batches */
   double ms_commit;        /* device time inside commit launches */
   double ms_setup;         /* store init + extrema */
+  int64_t disagreements;   /* GP_VERIFY=1 only: marked pairs a committed tree
+                              disagrees with (gp_run then returns GP_EDISAGREE) */
 } gp_run_stats;
 
 const char *gp_last_error(void);

@@ -35,6 +35,7 @@ class RunStats(ctypes.Structure):
         ("kernels", ctypes.c_int64), ("filled_pairs", ctypes.c_int64), ("visits", ctypes.c_int64),
         ("ms_total", ctypes.c_double), ("ms_propagate", ctypes.c_double),
         ("ms_commit", ctypes.c_double), ("ms_setup", ctypes.c_double),
+        ("disagreements", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

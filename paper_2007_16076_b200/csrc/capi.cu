@@ -40,7 +40,7 @@ struct gp_ctx {
   int isint;
   float* d_img = nullptr;
   cudaStream_t st = nullptr;
-  cudaStream_t st2 = nullptr;  // propagation stream (overlapped with the commit loop)
+  cudaStream_t st2 = nullptr;  // propagation stream of the host-driven (debug) loop
   cudaStream_t st3 = nullptr;  // device-to-host stream of completed D rows (gp_run_to_host)
   int border_n = -1;           // border source list resident in the workspace (its length)
   int* h_cnt = nullptr;        // pinned copy of the per-pixel counts
@@ -79,6 +79,18 @@ template <typename T>
 static cudaError_t dalloc(T** p, size_t count) {
   return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T) + 16);
 }
+
+// Scoped device buffer: freed on every return path (early CUDA_TRY returns
+// included).
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t alloc(size_t count) { return dalloc(&p, count); }
+};
 
 // Validate + convert host pixels to fp32 (grid.py:47-60 semantics).
 static int convert_pixels(int H, int W, int dtype, const void* pixels, int metric, int conn,
@@ -188,7 +200,8 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
 extern "C" int gp_ctx_num_pixels(const gp_ctx* c) { return c ? c->g.N : 0; }
 
 enum { WS_SEQ, WS_NEW, WS_SRC, WS_SLOT_OF, WS_RANK, WS_EXT, WS_SELKEY, WS_FLAGS, WS_CTL, WS_DFC,
-       WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK, WS_EXTK, WS_EXTT, WS_CSET };
+       WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK, WS_EXTK, WS_EXTT, WS_CSET,
+       WS_VERIFY };
 
 template <typename T>
 static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
@@ -245,27 +258,24 @@ extern "C" int gp_propagate(gp_ctx* c, const int32_t* sources, int nsrc, float* 
   }
   int rc = ensure_scratch(c, 1);
   if (rc) return rc;
-  int* d_src = nullptr;
-  float* d_dist = nullptr;
-  uint8_t* d_dir = nullptr;
-  CUDA_TRY(dalloc(&d_src, nsrc));
-  CUDA_TRY(dalloc(&d_dist, N));
-  CUDA_TRY(dalloc(&d_dir, N));
-  CUDA_TRY(cudaMemcpyAsync(d_src, sources, nsrc * 4, cudaMemcpyHostToDevice, c->st));
+  DevBuf<int> d_src;
+  DevBuf<float> d_dist;
+  DevBuf<uint8_t> d_dir;
+  CUDA_TRY(d_src.alloc(nsrc));
+  CUDA_TRY(d_dist.alloc(N));
+  CUDA_TRY(d_dir.alloc(N));
+  CUDA_TRY(cudaMemcpyAsync(d_src.p, sources, nsrc * 4, cudaMemcpyHostToDevice, c->st));
   PropArgs a = base_prop(c);
-  a.src = d_src;
+  a.src = d_src.p;
   a.ns = nsrc;
-  a.out_dist = d_dist;
-  a.out_dir = d_dir;
+  a.out_dist = d_dist.p;
+  a.out_dir = d_dir.p;
   a.delta = default_delta(c);
   CUDA_TRY(launch_propagate(a, 1, c->st));
   std::vector<uint8_t> dir(N);
-  if (dist_out) CUDA_TRY(cudaMemcpyAsync(dist_out, d_dist, N * 4, cudaMemcpyDeviceToHost, c->st));
-  CUDA_TRY(cudaMemcpyAsync(dir.data(), d_dir, N, cudaMemcpyDeviceToHost, c->st));
+  if (dist_out) CUDA_TRY(cudaMemcpyAsync(dist_out, d_dist.p, N * 4, cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaMemcpyAsync(dir.data(), d_dir.p, N, cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(cudaStreamSynchronize(c->st));
-  cudaFree(d_src);
-  cudaFree(d_dist);
-  cudaFree(d_dir);
   if (parent_out) {
     const int W = c->g.W;
     for (int v = 0; v < N; v++) {
@@ -382,12 +392,11 @@ static void ext_order(const std::vector<float>& dfc, std::vector<int32_t>& ext) 
 
 extern "C" int gp_extrema(gp_ctx* c, int32_t* centroid, float* dfc_out, int32_t* ext_out) {
   if (!c) return fail(GP_EINVAL, "null ctx");
-  float* d_dfc = nullptr;
-  CUDA_TRY(dalloc(&d_dfc, c->g.N));
+  DevBuf<float> d_dfc;
+  CUDA_TRY(d_dfc.alloc(c->g.N));
   std::vector<float> dfc;
   int cen = -1;
-  int rc = extrema_device(c, &cen, d_dfc, dfc);
-  cudaFree(d_dfc);
+  int rc = extrema_device(c, &cen, d_dfc.p, dfc);
   if (rc) return rc;
   std::vector<int32_t> ext;
   ext_order(dfc, ext);
@@ -447,21 +456,20 @@ extern "C" int gp_store_fill_tree(gp_store* s, const int32_t* parent, const floa
                                   float tol, int64_t* new_pairs) {
   if (!s || !parent || !tdist) return fail(GP_EINVAL, "null argument");
   const int N = (int)s->n;
-  int* d_par = nullptr;
-  float* d_td = nullptr;
-  CUDA_TRY(dalloc(&d_par, N));
-  CUDA_TRY(dalloc(&d_td, N));
-  CUDA_TRY(cudaMemcpyAsync(d_par, parent, N * 4, cudaMemcpyHostToDevice, s->st));
-  CUDA_TRY(cudaMemcpyAsync(d_td, tdist, N * 4, cudaMemcpyHostToDevice, s->st));
+  DevBuf<int> d_par;
+  DevBuf<float> d_td;
+  CUDA_TRY(d_par.alloc(N));
+  CUDA_TRY(d_td.alloc(N));
+  CUDA_TRY(cudaMemcpyAsync(d_par.p, parent, N * 4, cudaMemcpyHostToDevice, s->st));
+  CUDA_TRY(cudaMemcpyAsync(d_td.p, tdist, N * 4, cudaMemcpyHostToDevice, s->st));
   // snapshot so that a failed fill leaves the store unchanged is not needed by
-  // the reference (it also mutates before raising); mirror that behaviour.
+  // the reference (fill_tree_pairs mutates before the wrapper raises,
+  // _kernels.py:102-111, distances.py:108-116); mirror that behaviour.
   CUDA_TRY(cudaMemsetAsync(s->out3, 0, 24, s->st));
-  CUDA_TRY(launch_fill_tree_api(s->L, d_par, d_td, s->mark, s->cnt, s->D, s->out3, tol, s->st));
+  CUDA_TRY(launch_fill_tree_api(s->L, d_par.p, d_td.p, s->mark, s->cnt, s->D, s->out3, tol, s->st));
   unsigned long long o[3];
   CUDA_TRY(cudaMemcpyAsync(o, s->out3, 24, cudaMemcpyDeviceToHost, s->st));
   CUDA_TRY(cudaStreamSynchronize(s->st));
-  cudaFree(d_par);
-  cudaFree(d_td);
   if (o[2]) return fail(GP_ECYCLE, "tree parent links contain a cycle");
   if (o[1]) return fail(GP_EDISAGREE, "tree distances disagree with " + std::to_string(o[1]) +
                                           " already-stored entries");
@@ -476,17 +484,17 @@ extern "C" int gp_store_fill_source(gp_store* s, int64_t source, const float* di
   const int N = (int)s->n;
   if (source < 0 || source >= N) return fail(GP_EINVAL, "source out of range");
   if (dist[source] != 0.0f) return fail(GP_EINVAL, "source's distance to itself must be 0");
-  float* d_dist = nullptr;
-  CUDA_TRY(dalloc(&d_dist, N));
-  CUDA_TRY(cudaMemcpyAsync(d_dist, dist, N * 4, cudaMemcpyHostToDevice, s->st));
+  DevBuf<float> d_dist;
+  CUDA_TRY(d_dist.alloc(N));
+  CUDA_TRY(cudaMemcpyAsync(d_dist.p, dist, N * 4, cudaMemcpyHostToDevice, s->st));
   CUDA_TRY(cudaMemsetAsync(s->out3, 0, 24, s->st));
-  // the reference checks agreement before writing anything (distances.py:132-136)
-  CUDA_TRY(launch_fill_source_api(s->L, (int)source, d_dist, s->mark, s->cnt, s->D, s->out3,
+  // the reference checks agreement before writing anything (distances.py:132-136):
+  // a read-only check kernel runs first, the write kernel only without disagreements
+  CUDA_TRY(launch_fill_source_api(s->L, (int)source, d_dist.p, s->mark, s->cnt, s->D, s->out3,
                                   tol, s->st));
   unsigned long long o[3];
   CUDA_TRY(cudaMemcpyAsync(o, s->out3, 24, cudaMemcpyDeviceToHost, s->st));
   CUDA_TRY(cudaStreamSynchronize(s->st));
-  cudaFree(d_dist);
   if (o[1]) return fail(GP_EDISAGREE, "distance map disagrees with already-stored entries");
   s->filled += (int64_t)o[0];
   if (new_pairs) *new_pairs = (int64_t)o[0];
@@ -508,12 +516,11 @@ extern "C" int gp_store_read(gp_store* s, float* D_out, uint8_t* mark_out) {
   const size_t nn = (size_t)s->n * s->n;
   if (D_out) CUDA_TRY(cudaMemcpyAsync(D_out, s->D, nn * 4, cudaMemcpyDeviceToHost, s->st));
   if (mark_out) {
-    uint8_t* d_m = nullptr;
-    CUDA_TRY(dalloc(&d_m, nn));
-    CUDA_TRY(launch_mark_unpack(s->L, s->mark, d_m, s->st));
-    CUDA_TRY(cudaMemcpyAsync(mark_out, d_m, nn, cudaMemcpyDeviceToHost, s->st));
+    DevBuf<uint8_t> d_m;
+    CUDA_TRY(d_m.alloc(nn));
+    CUDA_TRY(launch_mark_unpack(s->L, s->mark, d_m.p, s->st));
+    CUDA_TRY(cudaMemcpyAsync(mark_out, d_m.p, nn, cudaMemcpyDeviceToHost, s->st));
     CUDA_TRY(cudaStreamSynchronize(s->st));
-    cudaFree(d_m);
   }
   CUDA_TRY(cudaStreamSynchronize(s->st));
   return GP_OK;
@@ -522,6 +529,24 @@ extern "C" int gp_store_read(gp_store* s, float* D_out, uint8_t* mark_out) {
 // ---------------- run_strategy ----------------
 struct EvPair {
   cudaEvent_t a, b;
+};
+
+// Events of one run: created checked, destroyed together when the run returns.
+struct EventPool {
+  std::vector<cudaEvent_t> ev;
+  EventPool() = default;
+  EventPool(const EventPool&) = delete;
+  EventPool& operator=(const EventPool&) = delete;
+  ~EventPool() { for (cudaEvent_t e : ev) cudaEventDestroy(e); }
+  cudaError_t make(cudaEvent_t* e, unsigned flags = cudaEventDefault) {
+    cudaError_t r = cudaEventCreateWithFlags(e, flags);
+    if (r == cudaSuccess) ev.push_back(*e);
+    return r;
+  }
+  cudaError_t pair(EvPair& p) {
+    cudaError_t r = make(&p.a);
+    return r == cudaSuccess ? make(&p.b) : r;
+  }
 };
 
 static float ev_ms(const EvPair& p) {
@@ -564,9 +589,9 @@ static int store_relayout(gp_store* s, const MarkLayout& L) {
 
 // Commit CTAs: two per SM when the loop has the GPU alone; one per SM when
 // propagation batches run concurrently on the other half of each SM.
-static int commit_blocks(gp_ctx* c, bool overlap) {
+static int commit_blocks(gp_ctx* c) {
   const int maxb = commit_max_blocks();
-  int bps = overlap ? 1 : 2048 / commit_threads();
+  int bps = 2048 / commit_threads();
   if (c->g.N < 16384) bps = 1;  // tiny fills: the barrier over fewer CTAs wins (64^2: 26.9 -> 25.0 ms)
   if (const char* e = getenv("GP_COMMIT_BLOCKS_PER_SM")) bps = atoi(e);
   return std::max(1, std::min(maxb, bps * c->nsm));
@@ -650,6 +675,8 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
                     int32_t* seq_out, int64_t* new_out, gp_run_stats* stats, float* D_host) {
   if (!c || !s) return fail(GP_EINVAL, "null argument");
   const int N = c->g.N;
+  EventPool evp;  // every event of the run, destroyed on all return paths
+  unsigned long long* d_verify = nullptr;  // GP_VERIFY disagreement counter
   RowStreamer rs{c, s, D_host, {}, 0};
   if (D_host) {
     rs.sent.assign(N, 0);
@@ -669,8 +696,8 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   if (rl) return rl;
   const MarkLayout L = s->L;
   EvPair tot, setup;
-  cudaEventCreate(&tot.a); cudaEventCreate(&tot.b);
-  cudaEventCreate(&setup.a); cudaEventCreate(&setup.b);
+  CUDA_TRY(evp.pair(tot));
+  CUDA_TRY(evp.pair(setup));
   const bool htime = getenv("GP_DEBUG_HOST") != nullptr;
   auto hnow = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   double h0 = hnow();
@@ -706,7 +733,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     CUDA_TRY(ws_get(c, WS_SRC, &d_src, N));
     CUDA_TRY(cudaMemcpyAsync(d_src, srcs.data(), (N - 1) * 4, cudaMemcpyHostToDevice, st));
     EvPair pp;
-    cudaEventCreate(&pp.a); cudaEventCreate(&pp.b);
+    CUDA_TRY(evp.pair(pp));
     CUDA_TRY(cudaEventRecord(pp.a, st));
     PropArgs a = base_prop(c);
     a.src = d_src;
@@ -723,20 +750,19 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     S.batches = 1;
     S.kernels += 2;
     P = N - 1;
-    cudaEventDestroy(pp.a); cudaEventDestroy(pp.b);
   } else {
     // ---- device commit loop with speculative propagation batches ----
-    // Default: commit launches and propagation batches alternate, each with the
-    // whole GPU.  GP_OVERLAP=1 runs the commit kernel on one CTA per SM and
-    // keeps a second stream producing the trees of the best unclaimed
-    // candidates on the other half of each SM (no kernel ever waits on another:
-    // the commit kernel leaves on a miss, K1 publishes a tree by writing
-    // slot_of[src] after it is complete).  Measured slower on B200 (both roles
-    // are latency/issue-bound and contend), so it is off by default.
+    // Commit launches and propagation batches alternate, each with the whole
+    // GPU.  (A concurrent propagation stream beside a one-CTA-per-SM commit
+    // kernel was measured slower in round 1 -- both roles are latency-bound
+    // and contend -- and removed: DESIGN.md section 5.)
     hmark("store reset");
-    const bool overlap = getenv("GP_OVERLAP") ? atoi(getenv("GP_OVERLAP")) != 0 : false;
-    commit_configure(overlap ? 0 : N);
-    const int nblocks = commit_blocks(c, overlap);
+    // GP_VERIFY=1: opt-in agreement check of every already-marked pair the
+    // committed trees revisit (reference _kernels.py:110-111): generic commit
+    // kernel, per-warp unit fill, no list mode, full rows not skipped
+    const bool verify = getenv("GP_VERIFY") && atoi(getenv("GP_VERIFY"));
+    commit_configure(N);
+    const int nblocks = commit_blocks(c);
     hmark("commit_blocks");
     int uf = N >= 32768 ? 3 : 1;  // work units per commit warp (measured at 256^2: 2 933, 3 915, 4 917, 8 1011 ms)
     if (const char* e = getenv("GP_UNITS_PER_WARP")) uf = std::max(1, atoi(e));
@@ -787,6 +813,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       const double capd = 64.0 * 1024 * 1024;  // list entries (256 MiB per buffer)
       h_ctl.list_switch = (unsigned long long)std::min(sw, capd);
       if (strategy != GP_STRATEGY_FILLING_RATE && !getenv("GP_LIST_ALPHA")) h_ctl.list_switch = 0;
+      if (verify) h_ctl.list_switch = 0;  // the list fill never revisits marked pairs
     }
     CUDA_TRY(cudaMemcpyAsync(d_ctl, &h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
     hmark("workspace");
@@ -808,9 +835,9 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     int K = spec_k > 0 ? spec_k : prop_trees_per_sm(N) * c->nsm;
     if (spec_k <= 0)
       if (const char* e = getenv("GP_SPEC_K")) K = atoi(e);
-    K = std::max(1, std::min(K, N));
-    int Q = overlap ? 2 * K : 0;  // lookahead bound of the concurrent batches
-    if (const char* e = getenv("GP_LOOKAHEAD")) Q = atoi(e);
+    // k_topk orders a batch's candidates (longest trees first) in a
+    // 1024-entry shared array: a batch holds at most 1024 trees
+    K = std::max(1, std::min({K, N, 1024}));
     CUDA_TRY(ws_get(c, WS_CANDS, &d_cands, K));
     CUDA_TRY(ws_get(c, WS_SLOTS, &d_slots, K));
     unsigned* d_tkeys = nullptr;
@@ -820,6 +847,15 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     CommitArgs ca;
     memset(&ca, 0, sizeof(ca));
     ca.fillq = getenv("GP_FILL_QUEUE") ? atoi(getenv("GP_FILL_QUEUE")) != 0 : 1;
+    ca.verify_corrupt = -1;
+    if (verify) {
+      ca.fillq = 0;
+      CUDA_TRY(ws_get(c, WS_VERIFY, &d_verify, 1));
+      CUDA_TRY(cudaMemsetAsync(d_verify, 0, 8, st));
+      ca.verify = d_verify;
+      ca.vtol = c->isint ? 0.0f : 1e-4f;
+      if (const char* e = getenv("GP_VERIFY_CORRUPT")) ca.verify_corrupt = atoi(e);
+    }
     ca.compact_div = 4;
     ca.lpt = getenv("GP_LPT") ? atoi(getenv("GP_LPT")) != 0 : 1;  // 256^2: 597 -> 587 ms, 128^2: 53.4 -> 51.9 ms
     if (const char* e = getenv("GP_COMPACT_DIV")) ca.compact_div = (unsigned)std::max(1, atoi(e));
@@ -858,7 +894,6 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     pa.publish = d_slot_of;
     pa.list_mode = &d_ctl->mode;  // trees made after the list switch skip pre/szp/partition
     pa.delta = default_delta(c);
-    pa.threads = overlap ? 512 : 0;
     const bool debug = getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"));
     unsigned long long* d_cdbg = nullptr;
     unsigned long long* d_pdbg = nullptr;
@@ -904,24 +939,20 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       }
     }
     std::vector<EvPair> pev, cev;
-    cudaEvent_t ev_c, ev_p;
-    cudaEventCreateWithFlags(&ev_c, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_p, cudaEventDisableTiming);
-    // one propagation batch on the propagation stream (lookahead q)
+    // one propagation batch on the propagation stream (host-driven loop)
     auto batch = [&](int q) -> int {
       EvPair f;
-      cudaEventCreate(&f.a); cudaEventCreate(&f.b);
+      CUDA_TRY(evp.pair(f));
       CUDA_TRY(cudaEventRecord(f.a, ps));
       CUDA_TRY(launch_topk(ca, K, q, d_cands, d_slots, d_tkeys, 0, ps));
       CUDA_TRY(launch_propagate(pa, K, ps));
       CUDA_TRY(cudaEventRecord(f.b, ps));
-      CUDA_TRY(cudaEventRecord(ev_p, ps));
       pev.push_back(f);
       S.batches++;
       S.kernels += 2;
       return GP_OK;
     };
-    const bool pipelined = !overlap && !debug && !(getenv("GP_PIPELINE") && !atoi(getenv("GP_PIPELINE")));
+    const bool pipelined = !debug && !(getenv("GP_PIPELINE") && !atoi(getenv("GP_PIPELINE")));
     if (pipelined) {
       // Device-gated pipeline: the host enqueues rounds of [commit, top-K,
       // propagation batch, list switch] on one stream; each kernel checks the
@@ -947,7 +978,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       const int chunk = 6;
       auto prop_batch = [&](int gated) -> int {
         EvPair f;
-        cudaEventCreate(&f.a); cudaEventCreate(&f.b);
+        CUDA_TRY(evp.pair(f));
         CUDA_TRY(cudaEventRecord(f.a, st));
         CUDA_TRY(launch_topk(ca, K, 0, d_cands, d_slots, d_tkeys, gated, st));
         CUDA_TRY(launch_propagate(pa, K, st));
@@ -958,7 +989,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       };
       auto round = [&]() -> int {  // one round: commit launch(es), batch, list switch
         EvPair e;
-        cudaEventCreate(&e.a); cudaEventCreate(&e.b);
+        CUDA_TRY(evp.pair(e));
         CUDA_TRY(cudaEventRecord(e.a, st));
         CUDA_TRY(commit_split() ? launch_commit_split(ca, nblocks, st) : launch_commit(ca, nblocks, st));
         CUDA_TRY(cudaEventRecord(e.b, st));
@@ -985,8 +1016,8 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
         if (!c->h_cnt2) CUDA_TRY(cudaHostAlloc(&c->h_cnt2, (size_t)2 * N * 4, cudaHostAllocDefault));
         if (!c->h_ctl2) CUDA_TRY(cudaHostAlloc(&c->h_ctl2, 2 * sizeof(Ctl), cudaHostAllocDefault));
         cudaEvent_t rev[2];
-        cudaEventCreateWithFlags(&rev[0], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&rev[1], cudaEventDisableTiming);
+        CUDA_TRY(evp.make(&rev[0], cudaEventDisableTiming));
+        CUDA_TRY(evp.make(&rev[1], cudaEventDisableTiming));
         auto end_round = [&](int b) -> int {
           CUDA_TRY(cudaMemcpyAsync(c->h_cnt2 + (size_t)b * N, s->cnt, (size_t)N * 4, cudaMemcpyDeviceToHost, st));
           CUDA_TRY(cudaMemcpyAsync(c->h_ctl2 + b, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -1010,15 +1041,13 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
           if (rs.open_rows >= 0 && rs.open_rows < N / 2 && e2e_cap > 0) ca.max_steps = e2e_cap;
         }
         CUDA_TRY(cudaStreamSynchronize(st));
-        cudaEventDestroy(rev[0]);
-        cudaEventDestroy(rev[1]);
         CUDA_TRY(cudaMemcpy(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
       }
       for (int guard = 0; !D_host && guard < 8 * N + 16; guard += chunk) {
         if (guard) rs.snapshot();  // quiescent point: the previous chunk is complete
         for (int it = 0; it < chunk; it++) {
           EvPair e;
-          cudaEventCreate(&e.a); cudaEventCreate(&e.b);
+          CUDA_TRY(evp.pair(e));
           CUDA_TRY(cudaEventRecord(e.a, st));
           CUDA_TRY(commit_split() ? launch_commit_split(ca, nblocks, st) : launch_commit(ca, nblocks, st));
           CUDA_TRY(cudaEventRecord(e.b, st));
@@ -1049,21 +1078,13 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     }
     for (int guard = 0; !pipelined && guard < 8 * N + 16; guard++) {
       EvPair e;
-      cudaEventCreate(&e.a); cudaEventCreate(&e.b);
+      CUDA_TRY(evp.pair(e));
       CUDA_TRY(cudaEventRecord(e.a, st));
       CUDA_TRY(commit_split() ? launch_commit_split(ca, nblocks, st) : launch_commit(ca, nblocks, st));
       CUDA_TRY(cudaEventRecord(e.b, st));
-      CUDA_TRY(cudaEventRecord(ev_c, st));
       cev.push_back(e);
       S.launches++;
       S.kernels++;
-      if (overlap) {  // keep the propagation stream busy while the commit loop runs
-        while (cudaEventQuery(ev_c) == cudaErrorNotReady) {
-          if (cudaEventQuery(ev_p) != cudaErrorNotReady) {
-            if (int r = batch(Q)) return r;
-          }
-        }
-      }
       CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
       if (h_ctl.status == CTL_DONE) break;
@@ -1159,12 +1180,17 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
         fprintf(stderr, "[gp debug] E5 offsets %.1f us, E6 arrays %.1f us\n", pacc[15] / 1e3 / pn, e6acc / 1e3 / pn);
       cudaFree(d_pdbg);
     }
-    for (auto& e : cev) { S.ms_commit += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
-    for (auto& e : pev) { S.ms_propagate += ev_ms(e); cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
-    cudaEventDestroy(ev_c);
-    cudaEventDestroy(ev_p);
+    for (auto& e : cev) S.ms_commit += ev_ms(e);
+    for (auto& e : pev) S.ms_propagate += ev_ms(e);
     P = h_ctl.step;
     S.propagations += h_ctl.total_props;
+    if (d_verify) {
+      unsigned long long bad = 0;
+      CUDA_TRY(cudaMemcpy(&bad, d_verify, 8, cudaMemcpyDeviceToHost));
+      S.disagreements = (int64_t)bad;
+      if (bad && !rc) rc = fail(GP_EDISAGREE, "verify: " + std::to_string(bad) +
+                                                  " already-stored entries disagree with a committed tree");
+    }
     S.visits = (int64_t)h_ctl.visits;
   }
   if (D_host && !rc) {
@@ -1182,8 +1208,6 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   S.ms_total = ev_ms(tot);
   S.ms_setup = ev_ms(setup);
   for (auto& m : hmarks) fprintf(stderr, "[gp host] %-24s %8.3f ms\n", m.first, m.second);
-  cudaEventDestroy(tot.a); cudaEventDestroy(tot.b);
-  cudaEventDestroy(setup.a); cudaEventDestroy(setup.b);
   if (rc) return rc;
   std::vector<unsigned long long> nw(P > 0 ? P : 1);
   if (P > 0) CUDA_TRY(cudaMemcpy(nw.data(), d_new, (size_t)P * 8, cudaMemcpyDeviceToHost));

@@ -164,6 +164,13 @@ __device__ __forceinline__ void set_mark(const CommitArgs& a, int row, uint32_t 
   atomicOr(a.mark + (size_t)row * a.L.RW + (col >> 5), 1u << (col & 31));
 }
 
+// verify mode: count a marked pair whose stored value disagrees with the
+// committed tree's (exact for integer images, relative vtol for fp32)
+__device__ __forceinline__ void verify_pair(const CommitArgs& a, float stored, float duv) {
+  if (fabsf(__fsub_rn(stored, duv)) > a.vtol * fmaxf(fabsf(duv), 1.0f))
+    atomicAdd(a.verify, 1ull);
+}
+
 // K2 for one committed tree: one work unit = chunks [b0, b1) of the tree's
 // chunk sequence (32 consecutive descendants of one preorder position).
 // The warp scans 32 preorder positions at a time (descendant counts, packed
@@ -172,9 +179,10 @@ __device__ __forceinline__ void set_mark(const CommitArgs& a, int row, uint32_t 
 // the inner loop is load entry -> load mark word of row u -> test bit, U
 // iterations in flight.  The fill is instruction-issue bound, so the loop is
 // kept to a handful of instructions per tested pair.
-template <int U>
+template <int U, bool VERIFY = false>
 __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int s, int p,
-                                          unsigned long long* sim = nullptr, unsigned* ustat = nullptr) {
+                                          unsigned long long* sim = nullptr, unsigned* ustat = nullptr,
+                                          bool corrupt = false) {
   const int N = a.g.N;
   const int lane = threadIdx.x & 31;
   const int P = a.ts.nparts;
@@ -215,7 +223,8 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
     const unsigned excl = cum - nch_l;
     const unsigned mych = excl < take ? min(nch_l, take - excl) : 0u;
     const int u_l = (int)(e_l & 0xFFFFu);
-    const bool full_l = mych && u_l != s && __ldcg(&a.cnt[u_l]) >= N - 1;
+    // (verify mode tests full rows too: their pairs are all compared)
+    const bool full_l = mych && u_l != s && !(VERIFY && a.verify) && __ldcg(&a.cnt[u_l]) >= N - 1;
     unsigned work = __ballot_sync(0xffffffffu, mych && !full_l);
     while (work) {
       const int ol = __ffs(work) - 1;
@@ -259,11 +268,16 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
             const int w = (int)(ew[j] & 0xFFFFu);
             set_mark(a, u, wcol);
             set_mark(a, w, ucol);
-            const float duv = __fsub_rn(__ldg(&tdp[qb + kb + 32u * j + lane]), __ldg(&tdp[qb - 1]));
+            float duv = __fsub_rn(__ldg(&tdp[qb + kb + 32u * j + lane]), __ldg(&tdp[qb - 1]));
+            if (VERIFY && corrupt) duv = __fadd_rn(duv, 1.0f);  // verify test hook
             a.D[(size_t)u * N + w] = duv;
             a.D[(size_t)w * N + u] = duv;
             atomicAdd(&a.cnt[w], 1);
             unew++;
+          } else if (VERIFY && a.verify && kb + 32u * j + lane < kend) {
+            const int w = (int)(ew[j] & 0xFFFFu);
+            const float duv = __fsub_rn(__ldg(&tdp[qb + kb + 32u * j + lane]), __ldg(&tdp[qb - 1]));
+            verify_pair(a, __ldcg(&a.D[(size_t)u * N + w]), duv);
           }
         }
       }
@@ -559,6 +573,7 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
 // row s is pixel-parallel over the whole grid; each unmarked column is a new
 // pair with D = td[x] - td[s] = tdp[tin[x]] - 0.  Bits of one mark word are
 // OR-ed by one lane per word (match_any).
+template <bool VERIFY = false>
 __device__ __forceinline__ unsigned fill_root_row(const CommitArgs& a, int slot, int s) {
   const int N = a.g.N;
   const MarkLayout L = a.L;
@@ -577,6 +592,8 @@ __device__ __forceinline__ unsigned fill_root_row(const CommitArgs& a, int slot,
     if (x < N && x != s) {
       xcol = mcol(L, (uint32_t)x);
       isnew = !(__ldcg(&row[xcol >> 5]) & (1u << (xcol & 31)));
+      if (VERIFY && !isnew && a.verify)
+        verify_pair(a, __ldcg(&a.D[(size_t)s * N + x]), __ldg(&tdp[__ldg(&tin[x]) & 0xFFFFu]));
     }
     const unsigned nm = __ballot_sync(0xffffffffu, isnew);
     if (!nm) continue;
@@ -807,7 +824,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
       const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
       if (PU <= nwarps) {  // one unit per warp: static
         const int u = (int)blockIdx.x * (int)(blockDim.x >> 5) + (int)(threadIdx.x >> 5);
-        if (u < PU) lnew = fill_unit<(G > 4 ? 4 : G)>(a, slot, s, u, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr);
+        if (u < PU) lnew = fill_unit<(G > 4 ? 4 : G), true>(a, slot, s, u, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr,
+                                                      nullptr, a.verify && step == a.verify_corrupt);
       } else {
         int* ctr = &unit_ctr[step & 1];
         int k = lane == 0 ? atomicAdd(ctr, 1) : 0;
@@ -818,7 +836,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
           int nk = lane == 0 ? atomicAdd(ctr, 1) : 0;
           unsigned* ust = (a.dbgu && step == a.dbgu_step) ? a.dbgu + (size_t)u * 8 : nullptr;
           const unsigned long long tu0 = ust ? gtimer() : 0ull;
-          lnew += fill_unit<(G > 4 ? 4 : G)>(a, slot, s, u, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr, ust);
+          lnew += fill_unit<(G > 4 ? 4 : G), true>(a, slot, s, u, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr, ust,
+                                             a.verify && step == a.verify_corrupt);
           if (ust && lane == 0) {
             ust[0] = (unsigned)(gtimer() - tu0);
             ust[5] = blockIdx.x;
@@ -830,7 +849,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
         if (threadIdx.x == 0) unit_ctr[(step & 1) ^ 1] = 0;  // next step's counter
       }
     }
-    if (mode == 0) lnew += fill_root_row(a, slot, s);
+    if (mode == 0) lnew += fill_root_row<!LEAN>(a, slot, s);
     if (dbg) dbg[1] = gtimer();
     if (!LEAN && a.dbgw && (threadIdx.x & 31) == 0) {
       const unsigned long long dt = gtimer() - tw0;
@@ -1035,6 +1054,7 @@ bool commit_split() {
   int v = getenv("GP_COMMIT_SPLIT") ? (atoi(getenv("GP_COMMIT_SPLIT")) != 0) : 1;
   // the split kernels carry no debug instrumentation and only the queue fill
   if ((getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"))) ||
+      (getenv("GP_VERIFY") && atoi(getenv("GP_VERIFY"))) ||
       (getenv("GP_FILL_QUEUE") && !atoi(getenv("GP_FILL_QUEUE"))))
     v = 0;
   return v != 0 && (commit_threads() == 1024 || commit_fill_depth() == 4);
@@ -1363,22 +1383,37 @@ cudaError_t launch_fill_tree_api(const MarkLayout& L, const int* parent, const f
   return cudaGetLastError();
 }
 
-// fill_from_source (distances.py:120-147): row and column of s.
+// fill_from_source (distances.py:120-147): row and column of s.  As in the
+// reference, the agreement of the already-marked entries is checked before
+// anything is written (distances.py:132-136): a read-only pass counts the
+// disagreements into out3[1], and the write pass does nothing when any.
+__global__ void k_fill_source_check(MarkLayout L, int s, const float* dist, const uint32_t* mark,
+                                    const float* D, unsigned long long* out3, float tol) {
+  const int N = L.N;
+  int bad = 0;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < N; x += gridDim.x * blockDim.x) {
+    if (x == s) continue;
+    const uint32_t xcol = mcol(L, (uint32_t)x);
+    if (mark[mword(L, (uint32_t)s, xcol)] & (1u << (xcol & 31))) {
+      const float val = dist[x], cur = D[(size_t)s * N + x];
+      if (fabsf(cur - val) > tol * fmaxf(fabsf(val), 1.0f)) bad++;
+    }
+  }
+  if (bad) atomicAdd(&out3[1], (unsigned long long)bad);
+}
+
 __global__ void k_fill_source_api(MarkLayout L, int s, const float* dist, uint32_t* mark,
                                   int* cnt, float* D, unsigned long long* out3, float tol) {
   const int N = L.N;
+  if (*(volatile unsigned long long*)&out3[1]) return;  // disagreement: store left unchanged
   const uint32_t scol = mcol(L, (uint32_t)s);
-  int lnew = 0, bad = 0;
+  int lnew = 0;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < N; x += gridDim.x * blockDim.x) {
     if (x == s) continue;
     const uint32_t xcol = mcol(L, (uint32_t)x);
     const uint32_t xbit = 1u << (xcol & 31);
     const float val = dist[x];
-    if (mark[mword(L, (uint32_t)s, xcol)] & xbit) {
-      float cur = D[(size_t)s * N + x];
-      if (fabsf(cur - val) > tol * fmaxf(fabsf(val), 1.0f)) bad++;
-      continue;
-    }
+    if (mark[mword(L, (uint32_t)s, xcol)] & xbit) continue;
     atomicOr(&mark[mword(L, (uint32_t)s, xcol)], xbit);
     atomicOr(&mark[mword(L, (uint32_t)x, scol)], 1u << (scol & 31));
     D[(size_t)s * N + x] = val;
@@ -1387,12 +1422,12 @@ __global__ void k_fill_source_api(MarkLayout L, int s, const float* dist, uint32
     lnew++;
   }
   if (lnew) { atomicAdd(&cnt[s], lnew); atomicAdd(&out3[0], (unsigned long long)lnew); }
-  if (bad) atomicAdd(&out3[1], (unsigned long long)bad);
 }
 
 cudaError_t launch_fill_source_api(const MarkLayout& L, int s, const float* dist, uint32_t* mark,
                                    int* cnt, float* D, unsigned long long* out3, float tol,
                                    cudaStream_t st) {
+  k_fill_source_check<<<(L.N + 255) / 256, 256, 0, st>>>(L, s, dist, mark, D, out3, tol);
   k_fill_source_api<<<(L.N + 255) / 256, 256, 0, st>>>(L, s, dist, mark, cnt, D, out3, tol);
   return cudaGetLastError();
 }

@@ -121,6 +121,13 @@ struct CommitArgs {
   unsigned compact_div;    // list mode: compact when dead entries > live / compact_div
   int lpt;                 // top-K: candidates deepest-first (longest trees first in the batch)
   unsigned long long total_pairs;
+  // opt-in agreement check (GP_VERIFY=1, generic kernel, per-warp unit fill,
+  // no list mode, full rows not skipped): marked pairs whose stored value
+  // differs from fl(td[w] - td[u]) by more than vtol * max(|value|, 1) are
+  // counted here (reference _kernels.py:110-111 -> distances.py:113-116)
+  unsigned long long* verify;
+  float vtol;
+  int verify_corrupt;      // test hook: new pairs of this step are stored +1 (-1: off)
 };
 
 void commit_configure(int N);

@@ -9,6 +9,8 @@ exist there):
     python tests/golden/make_golden.py cfg 2      # reference itself (int config)
     python tests/golden/make_golden.py cfg 4      # reference itself, force=True
     python tests/golden/make_golden.py cfg 1|3|5  # fp32 restatement (oracle/)
+    python tests/golden/make_golden.py trees 2    # reference: every source of cfg2
+    python tests/golden/make_golden.py trees 4    # reference: 256 sampled + first 64 committed
 
 Integer configs (2, 4) and every ``small`` case come from the UNMODIFIED
 reference package imported from /root/reference/pkg/src.  The reference
@@ -213,6 +215,43 @@ def make_cfg(index: int, nthreads: int):
     print(f"cfg{index}: raw={raw} adjusted={adjusted} elapsed={elapsed:.1f}s src={source}")
 
 
+def tree_digest(a: np.ndarray) -> np.ndarray:
+    """16-byte sha256 prefix of an int64 per-pixel array (dist or parent)."""
+    return np.frombuffer(hashlib.sha256(np.ascontiguousarray(a, dtype="<i8").tobytes()).digest()[:16],
+                         dtype=np.uint8)
+
+
+def make_trees(index: int):
+    """Predecessor identity at config scale: propagations of
+    the UNMODIFIED reference (GridGraph.propagate -> dijkstra_csr) on the config
+    image, stored as per-source digests of dist and parent (int64 LE):
+    cfg2 every source (4096), cfg4 256 seeded random sources plus the first 64
+    committed sources of the reference run (cfg4.npz seq)."""
+    gp = _ref()
+    spec = CONFIGS[index]
+    img = make_image(index)
+    graph = gp.GridGraph(gp.Image(img.astype(np.int64)), gp.Metric.SUM)
+    if index == 2:
+        srcs = np.arange(spec.n, dtype=np.int64)
+    else:
+        seq = np.load(os.path.join(HERE, f"cfg{index}.npz"))["seq"].astype(np.int64)
+        rnd = np.random.default_rng(9000 + index).choice(spec.n, 256, replace=False)
+        srcs = np.concatenate([seq[:64], rnd]).astype(np.int64)
+    t0 = time.time()
+    dd = np.zeros((len(srcs), 16), np.uint8)
+    pd = np.zeros((len(srcs), 16), np.uint8)
+    for i, s in enumerate(srcs):
+        r = graph.propagate([int(s)])
+        dd[i] = tree_digest(r.dist)
+        pd[i] = tree_digest(r.parent)
+    elapsed = time.time() - t0
+    np.savez_compressed(os.path.join(HERE, f"trees{index}.npz"), src=srcs.astype(np.int32),
+                        dist_digest=dd, parent_digest=pd,
+                        source=np.array("reference geopairs GridGraph.propagate"),
+                        cpu_seconds=np.array(elapsed))
+    print(f"trees{index}: {len(srcs)} sources in {elapsed:.1f}s")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "small":
         make_small()
@@ -220,5 +259,7 @@ if __name__ == "__main__":
         make_strategies()
     elif sys.argv[1] == "harness":
         make_harness()
+    elif sys.argv[1] == "trees":
+        make_trees(int(sys.argv[2]))
     else:
         make_cfg(int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 8)

@@ -108,6 +108,10 @@ def test_config_matches_golden(gp, index):
     assert run.trace.raw_count == int(g["raw"])
     assert run.trace.adjusted_count == int(g["adjusted"])
     assert np.array_equal(seq, g["seq"])
+    # per-commit new pairs (the reference's FillingTrace rates) and the extrema centroid
+    filled = np.array([int(f * spec.total_pairs) for _, _, f in run.trace.samples], dtype=np.int64)
+    assert np.array_equal(np.diff(np.concatenate([[0], filled])), g["new"])
+    assert int(run.stats["centroid"]) == int(g["centroid"])
     assert np.array_equal(run.distances.point_filled_counts, np.full(spec.n, spec.n - 1))
     isf = spec.dtype == "f32"
     Dd = run.distances.dist_device()

@@ -42,6 +42,23 @@ def test_small_runs_match_reference(ref_small, oracle):
             assert r["adjusted"] == int(c[tag + "_adj"])
 
 
+@pytest.mark.parametrize("index,stride", [(2, 1), (4, 1)])
+def test_config_trees_match_reference_digests(oracle, index, stride):
+    """The oracle's propagations on the config images against the reference's
+    own (tests/golden/trees*.npz: cfg2 every source, cfg4 320 sources)."""
+    g = load_golden(f"trees{index}.npz")
+    img = make_image(index)
+
+    def dig(a):
+        return np.frombuffer(hashlib.sha256(np.ascontiguousarray(a, dtype="<i8").tobytes()).digest()[:16],
+                             dtype=np.uint8)
+
+    for i in range(0, len(g["src"]), stride):
+        d, p = oracle.propagate(img, [int(g["src"][i])])
+        assert np.array_equal(dig(d), g["dist_digest"][i]), int(g["src"][i])
+        assert np.array_equal(dig(p), g["parent_digest"][i]), int(g["src"][i])
+
+
 def test_cfg2_matches_reference_run(oracle):
     g = load_golden("cfg2.npz")
     r = oracle.run(make_image(2), "filling-rate", nthreads=4)
