@@ -20,11 +20,15 @@ see DESIGN.md), value = N * A * K / max-over-ranks(device time of K steps).
   per image B_alg = 4N^2 + N^2/8 + C/4 + 10*N*P with C the
   ancestor/descendant pairs of the committed trees (measured on device),
   divided by the summed k_commit event time.
-* cpu_baseline / --impl reference: the oracle port (oracle/, C, OpenMP fill)
-  on the host cores, over a bounded prefix of the same run (the first M
-  commits of the GPU's own committed sequence, identical to the oracle's by
-  the parity tests); value = pairs filled by the prefix / prefix time, which
-  flatters the CPU (early commits fill the most pairs).
+* cpu_baseline (rank 0, N=1): the oracle port (oracle/, C; the reference
+  rejects fp32 images) on 1 host core -- the reference is single-threaded --
+  over the first M commits of the run, whole image extrapolated as per-commit
+  time x P (labelled); the port on all host threads beside it; the UNMODIFIED
+  reference (baseline/_ref, numba) on the integer configs: cfg2 whole image
+  measured, cfg4 a replayed prefix of the committed sequence, extrapolated.
+* --impl reference: the oracle port with all host threads, bounded prefix per
+  step, whole image extrapolated the same way; its `config` is built by the
+  same function as this arm's.
 """
 
 from __future__ import annotations
@@ -129,52 +133,113 @@ def _traffic(config: int, kernel: str):
         return None, None
 
 
-def _cpu_sample(img, spec, target_s: float, nthreads: int):
-    """The oracle port's real loop (selection + propagation + fill) for the
-    first M commits of the run, timed inside the loop (allocation excluded)."""
+def _golden_counts(index: int):
+    """P (raw, adjusted) of the committed sequence from the committed golden
+    fixture (equal to the GPU run's by the parity tests)."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", f"cfg{index}.npz"))
+    return int(g["raw"]), int(g["adjusted"])
+
+
+def _config_dict(spec, P: int, P_adj: int, world: int) -> dict:
+    """The `config` of both arms (identical by construction)."""
+    return {"workload": spec.name, "image": list(spec.shape), "connectivity": spec.conn,
+            "strategy": spec.strategy, "pairs_per_image": spec.total_pairs, "propagations_raw": P,
+            "propagations_adjusted": P_adj, "parallelism": f"replicas x{world}",
+            "l2": "flushed (256 MiB write) between steps"}
+
+
+def _port_sample(img, spec, P: int, target_s: float, nthreads: int):
+    """The oracle port's real loop (selection + propagation + tree fill) for
+    the first M commits of the run, timed inside the loop (allocation
+    excluded); the whole image is extrapolated as per-commit time x P (the
+    fill of every commit walks all ancestor pairs of its tree, reference
+    _kernels.py:96-115, so the per-commit cost is flat over the run)."""
     from oracle import oracle as O
 
-    m = min(spec.n, 8)
+    m = min(spec.n, 4)
     r = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m)
     per = r["loop_seconds"] / max(r["raw"], 1)
     m = int(min(spec.n, max(m, target_s / max(per, 1e-6))))
     r = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m)
-    dt, pairs = r["loop_seconds"], r["filled"]
+    dt, pairs, k = r["loop_seconds"], r["filled"], int(r["raw"])
+    per = dt / max(k, 1)
+    ms_image = per * P * 1e3
     return {
-        "value": pairs / dt, "unit": "pairs/s", "cores": nthreads, "kind": "port",
-        "sample": (f"oracle/oracle.c (C restatement of the reference loop, OpenMP fill) running the "
-                   f"first {r['raw']} commits of the {spec.name} filling-rate run: {pairs} of "
-                   f"{spec.total_pairs} pairs in {dt:.2f}s; the prefix rate flatters the CPU "
-                   "(early commits fill the most pairs)"),
-        "seconds": dt, "commits": int(r["raw"]),
+        "value": spec.total_pairs / (ms_image / 1e3), "unit": "pairs/s", "cores": nthreads,
+        "cores_available": os.cpu_count(), "kind": "port",
+        "ms_per_image": ms_image, "ms_per_image_kind": f"extrapolated: per-commit time of the first {k} commits x P={P}",
+        "per_commit_ms": per * 1e3, "commits_timed": k, "seconds": dt,
+        "prefix_pairs_per_s": pairs / dt,
+        "sample": (f"oracle/oracle.c (C restatement of the reference loop; the reference rejects fp32 images) "
+                   f"on {nthreads} of {os.cpu_count()} host threads: the first {k} commits of the "
+                   f"{spec.name} filling-rate run in {dt:.2f}s ({per * 1e3:.1f} ms per commit), whole image "
+                   f"extrapolated to {ms_image / 1e3:.0f}s for P={P} commits"),
     }
 
 
+def _ref_timing(mode: str, index: int, extra=None, timeout: float = 900.0):
+    """The UNMODIFIED reference (baseline/_ref, single-threaded numba) timed by
+    baseline/ref_timing.py in a subprocess."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "geopairs")):
+        return {"unavailable": "reference not installed in baseline/_ref (DESIGN.md section 9)"}
+    cmd = [sys.executable, os.path.join(ROOT, "baseline", "ref_timing.py"), mode, str(index)]
+    if extra is not None:
+        cmd.append(str(extra))
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+        line = [x for x in out.stdout.strip().splitlines() if x.startswith("{")][-1]
+        d = json.loads(line)
+        d["kind"] = "reference"
+        return d
+    except Exception as e:  # report, never fail the bench
+        return {"unavailable": f"reference timing failed: {type(e).__name__}: {e}"[:300]}
+
+
+def cpu_baseline(img, spec, index: int, P: int, target_s: float):
+    """cpu_baseline of the headline line (rank 0, N=1): the oracle port on 1
+    host core (the reference is single-threaded) with the whole image
+    extrapolated, the port on all host threads beside it, and the reference
+    itself on the integer configs (cfg2 whole image measured, cfg4 a replayed
+    prefix of the committed sequence, extrapolated)."""
+    one = _port_sample(img, spec, P, target_s, 1)
+    allt = _port_sample(img, spec, P, target_s, os.cpu_count() or 1)
+    one["port_all_threads"] = {k: allt[k] for k in ("value", "cores", "ms_per_image", "per_commit_ms",
+                                                     "commits_timed", "seconds", "prefix_pairs_per_s")}
+    one["reference_cfg2"] = _ref_timing("full", 2)
+    one["reference_cfg4"] = _ref_timing("replay", 4, 200)
+    return one
+
+
 def run_reference(args, spec, img, world, rank):
-    """--impl reference: the reference path's CPU implementation (oracle port)."""
+    """--impl reference: the reference path's CPU implementation on the host
+    cores -- the oracle port (the reference itself rejects the fp32 headline
+    image) with all host threads; each step a bounded prefix of the run, the
+    whole image extrapolated (per-commit time x P)."""
     if rank != 0:
         return
     nthreads = os.cpu_count() or 1
-    per_step = 15.0
-    vals = []
-    samples = []
+    P, P_adj = _golden_counts(args.config)
+    vals, samples = [], []
     for i in range(args.warmup + args.steps):
-        r = _cpu_sample(img, spec, per_step, nthreads)
+        r = _port_sample(img, spec, P, args.cpu_seconds, nthreads)
         if i >= args.warmup:
             vals.append(r["value"])
             samples.append(r)
     v = statistics.mean(vals)
-    ms = statistics.mean(s["seconds"] for s in samples) * 1e3
+    ms = statistics.mean(s["ms_per_image"] for s in samples)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if spec.dtype == "f32" else "f32(int-exact)",
-        "data": "synthetic", "config": {"workload": spec.name, "image": list(spec.shape),
-                                        "connectivity": spec.conn, "strategy": spec.strategy},
-        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": nthreads, "kind": "port",
-                         "sample": samples[-1]["sample"]},
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if spec.dtype == "f32" else "f32 (integer-exact)",
+        "data": "synthetic (seeded generator, paper_2007_16076_b200/configs.py)",
+        "config": _config_dict(spec, P, P_adj, world),
+        "cpu_baseline": {k: samples[-1][k] for k in ("value", "unit", "cores", "cores_available", "kind", "sample",
+                                                       "ms_per_image", "ms_per_image_kind", "per_commit_ms",
+                                                       "prefix_pairs_per_s")},
         "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    line["cpu_baseline"]["value"] = v
     print(json.dumps(line), flush=True)
 
 
@@ -227,7 +292,7 @@ def main():
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-others", action="store_true", help="skip the one-run summary of the other configs")
     args = ap.parse_args()
     world, rank, local = _dist_env()
@@ -332,10 +397,7 @@ def main():
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if spec.dtype == "f32" else "f32 (integer-exact)",
         "data": "synthetic (seeded generator, paper_2007_16076_b200/configs.py)",
-        "config": {"workload": spec.name, "image": list(spec.shape), "connectivity": spec.conn,
-                   "strategy": spec.strategy, "pairs_per_image": A, "propagations_raw": P,
-                   "propagations_adjusted": int(r0.adjusted_count),
-                   "parallelism": f"replicas x{world}", "l2": "flushed (256 MiB write) between steps"},
+        "config": _config_dict(spec, P, int(r0.adjusted_count), world),
         "e2e": {"value": world * A / e2e_s, "unit": "pairs/s", "ms_per_image": e2e_s * 1e3,
                 "h2d_bytes_per_step": int(px.nbytes), "d2h_bytes_per_step": 4 * N * N},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -357,7 +419,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_others:
         line["other_configs"] = _other_configs(L, _lib, args.config)
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = _cpu_sample(img, spec, args.cpu_seconds, os.cpu_count() or 1)
+        line["cpu_baseline"] = cpu_baseline(img, spec, args.config, P, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
     L.gp_store_destroy(st)

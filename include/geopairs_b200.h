@@ -24,10 +24,16 @@
  *   gp_store_fill_source DistanceArray.fill_from_source    distances.py:120-147
  *   gp_store_counts      DistanceArray.point_filled_counts distances.py:71-76
  *   gp_store_read        DistanceArray.dist / .mark        distances.py:55-58
- *   gp_run               run_strategy (naive, filling-rate) strategies.py:246-273
+ *   gp_store_apgd_rows   DistanceArray.to_bytes            distances.py:149-154
+ *   gp_store_load_rows   DistanceArray.from_bytes          distances.py:156-177
+ *   gp_store_recount     (from_bytes bookkeeping)          distances.py:174-176
+ *   gp_run               run_strategy (naive, filling-rate,  strategies.py:246-273
+ *                        extrema)                          (+ selectors :119-129,195-227)
  *   gp_run_to_host       run_strategy + DistanceArray.dist on the host, streamed
  *                        incl. _extrema_context            strategies.py:109-116
  *   gp_extrema           compute_extrema_context           strategies.py:104-116
+ *   gp_commit_source     one loop step of a host selector: propagate + build_tree +
+ *                        fill_from_tree                    strategies.py:263-271
  */
 #ifndef GEOPAIRS_B200_H
 #define GEOPAIRS_B200_H
@@ -51,7 +57,7 @@ enum {
 
 enum { GP_DTYPE_I64 = 0, GP_DTYPE_F32 = 1, GP_DTYPE_U8 = 2 };
 enum { GP_METRIC_L1 = 0, GP_METRIC_SUM = 1, GP_METRIC_MEAN = 2 };
-enum { GP_STRATEGY_NAIVE = 0, GP_STRATEGY_FILLING_RATE = 1 };
+enum { GP_STRATEGY_NAIVE = 0, GP_STRATEGY_FILLING_RATE = 1, GP_STRATEGY_EXTREMA = 2 };
 
 typedef struct gp_ctx gp_ctx;     /* image + grid graph + device tree store */
 typedef struct gp_store gp_store; /* device distance array D, mark bitmap, counts */
@@ -117,6 +123,30 @@ int gp_store_fill_source(gp_store *st, int64_t source, const float *dist, float 
 int gp_store_counts(gp_store *st, int32_t *counts_out, int64_t *filled_pairs);
 /* Host copies: D_out[n*n] fp32 (nullable), mark_out[n*n] bytes (nullable). */
 int gp_store_read(gp_store *st, float *D_out, uint8_t *mark_out);
+
+/* APGD dump (DistanceArray.to_bytes, distances.py:149-154):
+ * rows [row0, row0 + nrows) of the N x N u64 payload into host out[nrows * N],
+ * converted on the device (no N^2 host temporaries).  version 1 = the
+ * reference's format (integer distances); version 2 (additive, fp32 stores) =
+ * binary64 bits of each value.  Unmarked entries: all ones. */
+int gp_store_apgd_rows(gp_store *st, int version, int64_t row0, int64_t nrows, uint64_t *out);
+/* APGD load (DistanceArray.from_bytes, distances.py:156-177): rows of a
+ * payload into D and the mark bitmap (GP_EINVAL when a value does not fit the
+ * fp32 store exactly); then gp_store_recount. */
+int gp_store_load_rows(gp_store *st, int version, int64_t row0, int64_t nrows, const uint64_t *rows);
+/* Per-pixel counts and the filled-pair total recomputed from the mark bitmap
+ * (from_bytes: _point_filled = mark.sum(axis=0) - 1, distances.py:174-176). */
+int gp_store_recount(gp_store *st, int64_t *filled_pairs);
+
+/* One step of run_strategy's loop for a host-side selector (spiral,
+ * spiral-repulsion: strategies.py:132-192, 263-271): propagate from `source`
+ * (dijkstra_csr), fill its tree's ancestor/descendant pairs with the
+ * reference's agreement / cycle checks (fill_from_tree, distances.py:95-118;
+ * tol: relative, 0 = exact) and copy the per-pixel counts into counts_out[n]
+ * (host, nullable; pinned memory keeps it asynchronous) for the next
+ * selection.  One synchronisation per call, no allocation after the first. */
+int gp_commit_source(gp_ctx *ctx, gp_store *st, int32_t source, float tol, int64_t *new_pairs,
+                     int32_t *counts_out);
 
 /* run_strategy on the device.  seq_out[n] / new_out[n] receive the committed
  * sources and new pairs per commit (host, nullable); stats nullable.

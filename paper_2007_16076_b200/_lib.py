@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libgeopairs_b200.so")
 
 GP_OK, GP_EINVAL, GP_ENOMEM, GP_ECUDA, GP_EINTERNAL, GP_ECYCLE, GP_EDISAGREE, GP_EFULL = range(8)
 DTYPE_I64, DTYPE_F32, DTYPE_U8 = 0, 1, 2
-STRATEGY_NAIVE, STRATEGY_FILLING_RATE = 0, 1
+STRATEGY_NAIVE, STRATEGY_FILLING_RATE, STRATEGY_EXTREMA = 0, 1, 2
 
 # every symbol declared in include/geopairs_b200.h
 EXPORTS = (
@@ -23,7 +23,8 @@ EXPORTS = (
     "gp_ctx_num_pixels",
     "gp_propagate", "gp_propagate_batch", "gp_extrema", "gp_store_create", "gp_store_destroy",
     "gp_store_device_ptrs", "gp_store_fill_tree", "gp_store_fill_source", "gp_store_counts",
-    "gp_store_read", "gp_run", "gp_run_to_host",
+    "gp_store_read", "gp_store_apgd_rows", "gp_store_load_rows", "gp_store_recount",
+    "gp_commit_source", "gp_run", "gp_run_to_host",
 )
 
 
@@ -78,6 +79,10 @@ def load_library(path: str = LIB_PATH, *, require_device: bool = True):
     L.gp_store_fill_source.argtypes = [P, i64, P, f32, P]
     L.gp_store_counts.argtypes = [P, P, P]
     L.gp_store_read.argtypes = [P, P, P]
+    L.gp_store_apgd_rows.argtypes = [P, i32, i64, i64, P]
+    L.gp_store_load_rows.argtypes = [P, i32, i64, i64, P]
+    L.gp_store_recount.argtypes = [P, P]
+    L.gp_commit_source.argtypes = [P, P, i32, f32, P, P]
     L.gp_run.argtypes = [P, P, i32, i32, i32, P, P, ctypes.POINTER(RunStats)]
     L.gp_run_to_host.argtypes = [P, P, i32, i32, i32, P, P, ctypes.POINTER(RunStats), P]
     _lib = L

@@ -51,6 +51,7 @@ struct gp_ctx {
   size_t scratch_trees = 0;
   int commit_blocks = 0;
   double mean_w = 1.0;  // mean edge weight (bucket width scale)
+  int pos_w = 0;        // every edge weight > 0
   uint32_t* list[2] = {nullptr, nullptr};  // unfilled-pair lists (late phase)
   int* h_cnt2 = nullptr;     // pinned: two count snapshots (host-row rounds)
   Ctl* h_ctl2 = nullptr;     // pinned: two control-block snapshots
@@ -70,6 +71,8 @@ struct gp_store {
   unsigned long long* out3 = nullptr;
   int64_t filled = 0;
   cudaStream_t st = nullptr;
+  unsigned long long* stage = nullptr;  // APGD row-block staging (u64)
+  size_t stage_words = 0;
 };
 
 extern "C" const char* gp_last_error(void) { return g_err.c_str(); }
@@ -122,6 +125,26 @@ static int convert_pixels(int H, int W, int dtype, const void* pixels, int metri
   return GP_OK;
 }
 
+// Is every edge weight > 0?  (scaled_weight, grid.py:146-154: SUM/MEAN are
+// zero only between two zero pixels, L1 between equal pixels.)  Zero-weight
+// edges break the closed-form predecessor rule; the cluster K1 needs it.
+static int positive_weights(int H, int W, int conn, int metric, const std::vector<float>& f) {
+  for (int r = 0; r < H; r++)
+    for (int c = 0; c < W; c++) {
+      const float a = f[(size_t)r * W + c];
+      const int nb[4][2] = {{0, 1}, {1, -1}, {1, 0}, {1, 1}};
+      for (int k = 0; k < 4; k++) {
+        if (conn == 4 && (k == 1 || k == 3)) continue;
+        const int rr = r + nb[k][0], cc = c + nb[k][1];
+        if (rr >= H || cc < 0 || cc >= W) continue;
+        const float b = f[(size_t)rr * W + cc];
+        const bool zero = metric == GP_METRIC_L1 ? a == b : (a + b) == 0.0f;
+        if (zero) return 0;
+      }
+    }
+  return 1;
+}
+
 static double mean_weight(const std::vector<float>& f, int metric) {
   double s = 0;
   for (float v : f) s += v;
@@ -146,6 +169,7 @@ extern "C" int gp_ctx_create(int H, int W, int dtype, const void* pixels, int me
   c->g = make_grid(H, W, conn, metric);
   c->isint = isint;
   c->mean_w = mean_weight(f, metric);
+  c->pos_w = positive_weights(H, W, conn, metric, f);
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -168,6 +192,7 @@ extern "C" int gp_ctx_load(gp_ctx* c, int dtype, const void* pixels) {
   if (rc) return rc;
   c->isint = isint;
   c->mean_w = mean_weight(f, c->g.metric);
+  c->pos_w = positive_weights(c->g.H, c->g.W, c->g.conn, c->g.metric, f);
   CUDA_TRY(cudaMemcpyAsync(c->d_img, f.data(), (size_t)c->g.N * 4, cudaMemcpyHostToDevice, c->st));
   CUDA_TRY(cudaStreamSynchronize(c->st));
   return GP_OK;
@@ -201,7 +226,7 @@ extern "C" int gp_ctx_num_pixels(const gp_ctx* c) { return c ? c->g.N : 0; }
 
 enum { WS_SEQ, WS_NEW, WS_SRC, WS_SLOT_OF, WS_RANK, WS_EXT, WS_SELKEY, WS_FLAGS, WS_CTL, WS_DFC,
        WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK, WS_EXTK, WS_EXTT, WS_CSET,
-       WS_VERIFY };
+       WS_VERIFY, WS_CS_SRC, WS_CS_DIST, WS_CS_DIR, WS_CS_PAR };
 
 template <typename T>
 static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
@@ -219,11 +244,14 @@ static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
 }
 
 static int ensure_scratch(gp_ctx* c, size_t ntrees) {
-  if (prop_fits_smem(c->g.N) || ntrees <= c->scratch_trees) return GP_OK;
+  if (ntrees <= c->scratch_trees) return GP_OK;
+  // single-CTA global-scratch K1, or the overflow lists of the cluster K1
+  const size_t per = prop_fits_smem(c->g.N) ? prop_cluster_scratch(c->g.N)
+                                            : std::max(prop_scratch_bytes(c->g.N), prop_cluster_scratch(c->g.N));
   cudaFree(c->scratch);
   c->scratch = nullptr;
   c->scratch_trees = 0;
-  CUDA_TRY(dalloc(&c->scratch, prop_scratch_bytes(c->g.N) * ntrees));
+  CUDA_TRY(dalloc(&c->scratch, per * ntrees));
   c->scratch_trees = ntrees;
   return GP_OK;
 }
@@ -235,6 +263,7 @@ static PropArgs base_prop(gp_ctx* c) {
   a.img = c->d_img;
   a.scratch = c->scratch;
   a.delta = INFINITY;
+  a.pos_weights = c->pos_w;
   return a;
 }
 
@@ -438,8 +467,69 @@ extern "C" void gp_store_destroy(gp_store* s) {
   cudaFree(s->mark);
   cudaFree(s->cnt);
   cudaFree(s->out3);
+  cudaFree(s->stage);
   if (s->st) cudaStreamDestroy(s->st);
   delete s;
+}
+
+// ---------------- APGD (distances.py:149-177) ----------------
+// Row blocks of the u64 payload are converted on the device and copied in
+// slices of at most 32 MiB, so neither side ever holds an N^2 temporary.
+static const size_t kStageWords = (size_t)4 << 20;
+
+static int store_stage(gp_store* s) {
+  if (s->stage) return GP_OK;
+  CUDA_TRY(dalloc(&s->stage, kStageWords));
+  s->stage_words = kStageWords;
+  return GP_OK;
+}
+
+extern "C" int gp_store_apgd_rows(gp_store* s, int version, int64_t row0, int64_t nrows, uint64_t* out) {
+  if (!s || !out) return fail(GP_EINVAL, "null argument");
+  if (version != 1 && version != 2) return fail(GP_EINVAL, "unsupported APGD version");
+  if (row0 < 0 || nrows < 0 || row0 + nrows > s->n) return fail(GP_EINVAL, "row range out of bounds");
+  if (int rc = store_stage(s)) return rc;
+  const int64_t n = s->n;
+  const int64_t per = std::max<int64_t>(1, (int64_t)(s->stage_words / (size_t)n));
+  for (int64_t r = row0; r < row0 + nrows; r += per) {
+    const int64_t k = std::min(per, row0 + nrows - r);
+    CUDA_TRY(launch_apgd_dump(s->L, s->D, s->mark, r, k, version, s->stage, s->st));
+    CUDA_TRY(cudaMemcpyAsync(out + (r - row0) * n, s->stage, (size_t)(k * n) * 8, cudaMemcpyDeviceToHost, s->st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->st));
+  return GP_OK;
+}
+
+extern "C" int gp_store_load_rows(gp_store* s, int version, int64_t row0, int64_t nrows, const uint64_t* rows) {
+  if (!s || !rows) return fail(GP_EINVAL, "null argument");
+  if (version != 1 && version != 2) return fail(GP_EINVAL, "unsupported APGD version");
+  if (row0 < 0 || nrows < 0 || row0 + nrows > s->n) return fail(GP_EINVAL, "row range out of bounds");
+  if (int rc = store_stage(s)) return rc;
+  const int64_t n = s->n;
+  const int64_t per = std::max<int64_t>(1, (int64_t)(s->stage_words / (size_t)n));
+  CUDA_TRY(cudaMemsetAsync(s->out3, 0, 24, s->st));
+  for (int64_t r = row0; r < row0 + nrows; r += per) {
+    const int64_t k = std::min(per, row0 + nrows - r);
+    CUDA_TRY(cudaMemcpyAsync(s->stage, rows + (r - row0) * n, (size_t)(k * n) * 8, cudaMemcpyHostToDevice, s->st));
+    CUDA_TRY(launch_apgd_load(s->L, s->D, s->mark, r, k, version, s->stage, s->out3 + 1, s->st));
+  }
+  unsigned long long bad = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bad, s->out3 + 1, 8, cudaMemcpyDeviceToHost, s->st));
+  CUDA_TRY(cudaStreamSynchronize(s->st));
+  if (bad) return fail(GP_EINVAL, std::to_string(bad) + " APGD values are not representable in the fp32 store");
+  return GP_OK;
+}
+
+extern "C" int gp_store_recount(gp_store* s, int64_t* filled) {
+  if (!s) return fail(GP_EINVAL, "null store");
+  CUDA_TRY(cudaMemsetAsync(s->out3, 0, 24, s->st));
+  CUDA_TRY(launch_store_recount(s->L, s->mark, s->cnt, s->out3, s->st));
+  unsigned long long marks = 0;
+  CUDA_TRY(cudaMemcpyAsync(&marks, s->out3, 8, cudaMemcpyDeviceToHost, s->st));
+  CUDA_TRY(cudaStreamSynchronize(s->st));
+  s->filled = ((int64_t)marks - s->n) / 2;
+  if (filled) *filled = s->filled;
+  return GP_OK;
 }
 
 extern "C" int gp_store_device_ptrs(gp_store* s, float** D, uint32_t** mark, int32_t** counts,
@@ -523,6 +613,46 @@ extern "C" int gp_store_read(gp_store* s, float* D_out, uint8_t* mark_out) {
     CUDA_TRY(cudaStreamSynchronize(s->st));
   }
   CUDA_TRY(cudaStreamSynchronize(s->st));
+  return GP_OK;
+}
+
+// ---------------- host-selected strategies: one commit per call ----------------
+extern "C" int gp_commit_source(gp_ctx* c, gp_store* s, int32_t source, float tol, int64_t* new_pairs,
+                                int32_t* counts_out) {
+  if (!c || !s) return fail(GP_EINVAL, "null argument");
+  const int N = c->g.N;
+  if (s->n != N) return fail(GP_EINVAL, "store size does not match the image");
+  if (source < 0 || source >= N) return fail(GP_EINVAL, "source out of range");
+  if (int rc = ensure_scratch(c, 1)) return rc;
+  int *d_src = nullptr, *d_par = nullptr;
+  float* d_dist = nullptr;
+  uint8_t* d_dir = nullptr;
+  CUDA_TRY(ws_get(c, WS_CS_SRC, &d_src, 1));
+  CUDA_TRY(ws_get(c, WS_CS_DIST, &d_dist, N));
+  CUDA_TRY(ws_get(c, WS_CS_DIR, &d_dir, N));
+  CUDA_TRY(ws_get(c, WS_CS_PAR, &d_par, N));
+  CUDA_TRY(cudaStreamSynchronize(s->st));  // earlier store calls complete
+  cudaStream_t st = c->st;
+  CUDA_TRY(cudaMemcpyAsync(d_src, &source, 4, cudaMemcpyHostToDevice, st));
+  PropArgs a = base_prop(c);
+  a.src = d_src;
+  a.ns = 1;
+  a.out_dist = d_dist;
+  a.out_dir = d_dir;
+  a.delta = default_delta(c);
+  CUDA_TRY(launch_propagate(a, 1, st));
+  CUDA_TRY(launch_dir_to_parent(d_dir, N, c->g.W, d_par, st));
+  CUDA_TRY(cudaMemsetAsync(s->out3, 0, 24, st));
+  CUDA_TRY(launch_fill_tree_api(s->L, d_par, d_dist, s->mark, s->cnt, s->D, s->out3, tol, st));
+  unsigned long long o[3];
+  CUDA_TRY(cudaMemcpyAsync(o, s->out3, 24, cudaMemcpyDeviceToHost, st));
+  if (counts_out) CUDA_TRY(cudaMemcpyAsync(counts_out, s->cnt, (size_t)N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (o[2]) return fail(GP_ECYCLE, "tree parent links contain a cycle");
+  if (o[1]) return fail(GP_EDISAGREE, "tree distances disagree with " + std::to_string(o[1]) +
+                                          " already-stored entries");
+  s->filled += (int64_t)o[0];
+  if (new_pairs) *new_pairs = (int64_t)o[0];
   return GP_OK;
 }
 
@@ -684,7 +814,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     if (!c->h_cnt) CUDA_TRY(cudaHostAlloc(&c->h_cnt, (size_t)N * 4, cudaHostAllocDefault));
   }
   if (s->n != N) return fail(GP_EINVAL, "store size does not match the image");
-  if (strategy != GP_STRATEGY_NAIVE && strategy != GP_STRATEGY_FILLING_RATE)
+  if (strategy != GP_STRATEGY_NAIVE && strategy != GP_STRATEGY_FILLING_RATE && strategy != GP_STRATEGY_EXTREMA)
     return fail(GP_EINVAL, "strategy not supported on the device path");
   cudaStream_t st = c->st;
   gp_run_stats S;
@@ -812,13 +942,13 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       double sw = alpha * est_tree;
       const double capd = 64.0 * 1024 * 1024;  // list entries (256 MiB per buffer)
       h_ctl.list_switch = (unsigned long long)std::min(sw, capd);
-      if (strategy != GP_STRATEGY_FILLING_RATE && !getenv("GP_LIST_ALPHA")) h_ctl.list_switch = 0;
+      if (strategy == GP_STRATEGY_NAIVE && !getenv("GP_LIST_ALPHA")) h_ctl.list_switch = 0;
       if (verify) h_ctl.list_switch = 0;  // the list fill never revisits marked pairs
     }
     CUDA_TRY(cudaMemcpyAsync(d_ctl, &h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
     hmark("workspace");
     int* d_cen = nullptr;
-    if (strategy == GP_STRATEGY_FILLING_RATE) {
+    if (strategy != GP_STRATEGY_NAIVE) {  // _extrema_context (strategies.py:109-116)
       int r = extrema_async(c, &d_cen, d_dfc);
       if (r) return r;
       unsigned long long* d_ek = nullptr;
@@ -829,6 +959,10 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       CUDA_TRY(launch_ext_rank(d_dfc, N, d_ek, d_et, tb, d_ext, d_rank, st));
       S.propagations += 2;
       S.kernels += 6;
+      if (strategy == GP_STRATEGY_EXTREMA) {  // key part: first position of the distance class
+        CUDA_TRY(launch_group_start(d_dfc, d_ext, N, d_rank, st));
+        S.kernels += 1;
+      }
     }
     hmark("extrema+rank enqueued");
     CUDA_TRY(cudaEventRecord(setup.b, st));
@@ -867,7 +1001,8 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     }
     ca.g = c->g;
     ca.L = L;
-    ca.strategy = strategy == GP_STRATEGY_FILLING_RATE ? kFillingRate : kNaive;
+    ca.strategy = strategy == GP_STRATEGY_FILLING_RATE ? kFillingRate
+                : strategy == GP_STRATEGY_EXTREMA ? kExtrema : kNaive;
     ca.ts = c->ts;
     ca.slot_of = d_slot_of;
     ca.claimed = d_claimed;
@@ -894,6 +1029,12 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     pa.publish = d_slot_of;
     pa.list_mode = &d_ctl->mode;  // trees made after the list switch skip pre/szp/partition
     pa.delta = default_delta(c);
+    DevBuf<unsigned long long> cl_dbg;  // GP_CL_DEBUG: cluster-K1 phase sums
+    if (getenv("GP_CL_DEBUG") && atoi(getenv("GP_CL_DEBUG"))) {
+      CUDA_TRY(cl_dbg.alloc(16));
+      CUDA_TRY(cudaMemsetAsync(cl_dbg.p, 0, 16 * 8, st));
+      pa.cl_dbg = cl_dbg.p;
+    }
     const bool debug = getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"));
     unsigned long long* d_cdbg = nullptr;
     unsigned long long* d_pdbg = nullptr;
@@ -1184,6 +1325,16 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     for (auto& e : pev) S.ms_propagate += ev_ms(e);
     P = h_ctl.step;
     S.propagations += h_ctl.total_props;
+    if (cl_dbg.p) {
+      unsigned long long h[16];
+      CUDA_TRY(cudaMemcpy(h, cl_dbg.p, sizeof(h), cudaMemcpyDeviceToHost));
+      const double nt = h[13] ? (double)h[13] : 1.0;
+      fprintf(stderr, "[gp cluster K1] per tree (us): relax %.1f parents %.1f upsweep %.1f sizes %.1f "
+              "e5 %.1f jump %.1f e6a %.1f rest %.1f | passes %.1f advances %.1f jumps %.1f (trees %llu, lite %llu)\n",
+              h[1] / nt / 1e3, h[2] / nt / 1e3, h[3] / nt / 1e3, h[4] / nt / 1e3, h[5] / nt / 1e3,
+              h[6] / nt / 1e3, h[7] / nt / 1e3, h[8] / nt / 1e3, h[10] / nt, h[11] / nt, h[12] / nt,
+              h[13], h[14]);
+    }
     if (d_verify) {
       unsigned long long bad = 0;
       CUDA_TRY(cudaMemcpy(&bad, d_verify, 8, cudaMemcpyDeviceToHost));
@@ -1219,7 +1370,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   }
   s->filled = filled;
   S.raw_count = P;
-  S.adjusted_count = P + (strategy == GP_STRATEGY_FILLING_RATE ? 2 : 0);
+  S.adjusted_count = P + (strategy != GP_STRATEGY_NAIVE ? 2 : 0);  // EXTREMA_OVERHEAD
   S.filled_pairs = filled;
   if (stats) *stats = S;
   const int64_t total = ((int64_t)N * N - N) / 2;

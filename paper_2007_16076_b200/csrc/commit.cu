@@ -42,14 +42,30 @@ namespace cg = cooperative_groups;
 
 namespace gp {
 
+// Selection key (smaller wins; equal keys: smaller pixel id, by the packing
+// of sel_pack).  `rank` is the strategy's static per-pixel part:
+//   filling-rate (strategies.py:220-227): count, then greatest distance from
+//     the centroid, then smallest id:  count << 16 | rank, rank = position in
+//     ext = lexsort((id, -dist_from_c));
+//   extrema (strategies.py:203-210): greatest distance from the centroid,
+//     then least filled, then smallest id:  gs << 16 | count, gs = first
+//     position of v's distance class in ext (ties of equal distance share it);
+//   naive with tree (strategies.py:125-129): smallest open id.
+// Keys only grow (counts only increase), which the candidate set relies on.
 __device__ __forceinline__ unsigned sel_key(int strategy, int N, int v, int c, const int* rank) {
   if (c >= N - 1) return 0xFFFFFFFFu;
   if (strategy == kFillingRate) return ((unsigned)c << 16) | (unsigned)__ldg(&rank[v]);
+  if (strategy == kExtrema) return ((unsigned)__ldg(&rank[v]) << 16) | (unsigned)c;
   return (unsigned)v;
 }
 
-__device__ __forceinline__ int key_src(int strategy, unsigned key, const int* ext) {
-  return strategy == kFillingRate ? __ldg(&ext[key & 0xFFFFu]) : (int)key;
+// the static part of a key (kept in the candidate set) and the key rebuilt
+// from it with a current count
+__device__ __forceinline__ unsigned key_static(int strategy, unsigned key) {
+  return strategy == kExtrema ? key >> 16 : key & 0xFFFFu;
+}
+__device__ __forceinline__ unsigned key_with_count(int strategy, unsigned stat, int c) {
+  return strategy == kExtrema ? (stat << 16) | (unsigned)c : ((unsigned)c << 16) | stat;
 }
 
 template <typename T>
@@ -144,7 +160,7 @@ __device__ void select_collect(const CommitArgs& a, int step, int skip, unsigned
       if ((threadIdx.x & 31) == 0) base = atomicAdd(&a.ctl->cand_cnt[step & 1], (unsigned)__popc(bm));
       base = __shfl_sync(0xffffffffu, base, 0);
       const unsigned pos = base + __popc(bm & ((1u << (threadIdx.x & 31)) - 1u));
-      if (in && pos < (unsigned)CAND_CAP) a.cand[pos] = (uint32_t)v | ((key & 0xFFFFu) << 16);
+      if (in && pos < (unsigned)CAND_CAP) a.cand[pos] = (uint32_t)v | (key_static(a.strategy, key) << 16);
     }
   }
   m = block_reduce_min(m, red64);
@@ -749,11 +765,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   __shared__ unsigned long long red64[32];
   __shared__ int unit_ctr[2];  // per-CTA work-unit counters (alternating steps)
   __shared__ FillQ fq;         // per-CTA chunk queue (tree mode)
-  __shared__ uint32_t cand_s[CAND_CAP];  // candidate set: pixel | rank << 16
+  __shared__ uint32_t cand_s[CAND_CAP];  // candidate set: pixel | static key part << 16
   __shared__ unsigned long long sel_s;   // fast-path selection broadcast
   // candidate-set state, CTA-uniform (shared memory, not registers)
   __shared__ unsigned cand_n, cand_T, cand_delta, cur_key;
-  const bool use_cand = a.cand != nullptr && a.strategy == kFillingRate;
+  const bool use_cand = a.cand != nullptr && a.strategy != kNaive;
   if (threadIdx.x == 0) {
     unit_ctr[0] = unit_ctr[1] = 0;
     fq.n = fq.res = fq.head = 0;
@@ -894,7 +910,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
         if (v == s) continue;
         const int c = __ldcg(&a.cnt[v]);
         const int sl = __ldcg(&a.slot_of[v]);
-        if (c < N - 1) m = min(m, sel_pack(((unsigned)c << 16) | (e >> 16), v, sl));
+        if (c < N - 1) m = min(m, sel_pack(key_with_count(a.strategy, e >> 16, c), v, sl));
       }
       m = block_reduce_min(m, red64);
       if (threadIdx.x == 0) sel_s = m;
@@ -1374,6 +1390,17 @@ __global__ void k_fill_tree_api(MarkLayout L, const int* parent, const float* td
     if (lnew) { atomicAdd(&cnt[v], lnew); atomicAdd(&out3[0], (unsigned long long)lnew); }
     if (bad) atomicAdd(&out3[1], (unsigned long long)bad);
   }
+}
+
+// 3x3 window codes of a propagation -> parent ids (-1 for roots)
+__global__ void k_dir_to_parent(const uint8_t* dir, int N, int W, int* parent) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x)
+    parent[v] = parent_of(v, dir[v], W);
+}
+
+cudaError_t launch_dir_to_parent(const uint8_t* dir, int N, int W, int* parent, cudaStream_t st) {
+  k_dir_to_parent<<<(N + 255) / 256, 256, 0, st>>>(dir, N, W, parent);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fill_tree_api(const MarkLayout& L, const int* parent, const float* tdist,

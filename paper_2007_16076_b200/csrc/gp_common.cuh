@@ -18,7 +18,7 @@
 namespace gp {
 
 enum Metric : int { kL1 = 0, kSum = 1, kMean = 2 };
-enum Strategy : int { kNaive = 0, kFillingRate = 1 };
+enum Strategy : int { kNaive = 0, kFillingRate = 1, kExtrema = 2 };
 
 constexpr uint8_t GP_ROOT = 0xFF;
 constexpr uint32_t INF_BITS = 0x7F800000u;  // +inf; non-negative floats order as uint32

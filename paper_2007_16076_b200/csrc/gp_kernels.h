@@ -51,6 +51,8 @@ struct PropArgs {
   int* publish;            // optional slot_of[]: set slot_of[src] = slot once the tree is written
   int threads;             // CTA size override (0: automatic)
   const int* list_mode;    // optional &Ctl::mode: == 1 -> list-mode tree (tin/tdp/C only)
+  int pos_weights;         // every edge weight > 0 (closed-form parents; cluster K1 allowed)
+  unsigned long long* cl_dbg;  // optional cluster-K1 phase time sums [16] (GP_CL_DEBUG)
 };
 
 size_t prop_smem_bytes(int N);
@@ -58,6 +60,11 @@ size_t prop_scratch_bytes(int N);
 bool prop_fits_smem(int N);
 int prop_trees_per_sm(int N);
 cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st);
+// cluster variant (propagate_cluster.cu): one tree per 2-CTA cluster, state in DSMEM
+size_t prop_cluster_smem(int N);
+size_t prop_cluster_scratch(int N);
+bool prop_cluster_ok(int N);
+cudaError_t launch_propagate_cluster(const PropArgs& a, int ntrees, cudaStream_t st);
 
 // ---------------- K2/K3 commit loop ----------------
 struct Ctl {
@@ -93,14 +100,14 @@ struct GridBarrier {
 struct CommitArgs {
   Grid g;
   MarkLayout L;
-  int strategy;            // kNaive (naive_with_tree) or kFillingRate
+  int strategy;            // kNaive (naive_with_tree), kFillingRate or kExtrema
   TreeStore ts;
   int* slot_of;            // [N] slot of a pixel's tree, -1 none (or in flight), -2 committed
   uint8_t* claimed;        // [N] 1 once a pixel is handed to a propagation batch
   uint32_t* mark;          // [N][RW] bitmap
   int* cnt;                // [N] marked off-diagonal entries per pixel
   float* D;                // [N][N]
-  const int* rank;         // [N] position in the extrema ranking (filling-rate)
+  const int* rank;         // [N] static key part: rank in ext (filling-rate) / class start (extrema)
   const int* ext;          // [N] pixel at each rank
   unsigned long long* selkey;  // [N+2] per-step packed selection (atomicMin target)
   unsigned* stepflags;     // [N+2] per-step decisions from the bookkeeping thread
@@ -149,6 +156,9 @@ cudaError_t launch_store_init(const MarkLayout& L, uint32_t* mark, float* D, cud
 size_t ext_rank_temp_bytes(int N);
 cudaError_t launch_ext_rank(const float* dfc, int N, unsigned long long* keys2, void* temp,
                             size_t temp_bytes, int* ext, int* rank, cudaStream_t st);
+// extrema selection key: first position of each pixel's distance class in ext
+cudaError_t launch_group_start(const float* dfc, const int* ext, int N, int* gs, cudaStream_t st);
+cudaError_t launch_dir_to_parent(const uint8_t* dir, int N, int W, int* parent, cudaStream_t st);
 // API-level fills (explicit parent arrays; reference semantics incl. checks)
 cudaError_t launch_fill_tree_api(const MarkLayout& L, const int* parent, const float* tdist,
                                  uint32_t* mark, int* cnt, float* D, unsigned long long* out3,
@@ -161,6 +171,14 @@ cudaError_t launch_mark_unpack(const MarkLayout& L, const uint32_t* mark, uint8_
 cudaError_t launch_naive_trace(const MarkLayout& L, uint32_t* mark, int* cnt, int* seq,
                                unsigned long long* newp, cudaStream_t st);
 cudaError_t launch_argmax_first(const float* x, int N, int* out, cudaStream_t st);
+// APGD (apgd.cu): device-side u64 conversion of row blocks, load, recount
+cudaError_t launch_apgd_dump(const MarkLayout& L, const float* D, const uint32_t* mark, long long row0,
+                             long long nrows, int version, unsigned long long* out, cudaStream_t st);
+cudaError_t launch_apgd_load(const MarkLayout& L, float* D, uint32_t* mark, long long row0, long long nrows,
+                             int version, const unsigned long long* in, unsigned long long* bad,
+                             cudaStream_t st);
+cudaError_t launch_store_recount(const MarkLayout& L, const uint32_t* mark, int* cnt,
+                                 unsigned long long* marks, cudaStream_t st);
 cudaError_t launch_build_list(const MarkLayout& L, const uint32_t* mark, uint32_t* list,
                               unsigned* count, cudaStream_t st);
 

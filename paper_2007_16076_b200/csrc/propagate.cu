@@ -1061,8 +1061,26 @@ int prop_trees_per_sm(int N) {
   return std::max(1, per_sm);
 }
 
+// The cluster K1 (propagate_cluster.cu) can take the speculative batches of
+// maps above one SM's shared memory when every edge weight is positive (its
+// predecessor rule has no plateau pass): GP_PROP_CLUSTER=1.  Measured slower
+// than the single-CTA global-scratch variant at 256^2,
+// so off by default; GP_PROP_CLUSTER=2 also sends maps that fit one SM to it
+// (tests).
+static bool use_cluster(const PropArgs& a) {
+  const char* e = getenv("GP_PROP_CLUSTER");
+  const int knob = e ? atoi(e) : 0;
+  if (!knob || (prop_fits_smem(a.g.N) && knob != 2)) return false;
+  if (!a.pos_weights || a.ns != 1 || !a.ts.pre) return false;
+  if (a.dbg || a.D || a.out_dist || a.out_dir) return false;
+  static int ok = -1;
+  if (ok < 0) ok = prop_cluster_ok(a.g.N) ? 1 : 0;
+  return ok == 1;
+}
+
 cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st) {
   if (ntrees <= 0) return cudaSuccess;
+  if (use_cluster(a)) return launch_propagate_cluster(a, ntrees, st);
   a.in_smem = prop_fits_smem(a.g.N) ? 1 : 0;
   if (!a.in_smem) a.scratch_bytes = prop_scratch_bytes(a.g.N);
   const size_t smem = prop_dyn_smem(a.g.N);

@@ -25,6 +25,37 @@ __global__ void k_ext_rank(const unsigned long long* sorted, int N, int* ext, in
   }
 }
 
+// Extrema key (strategies.py:203-210): gs[v] = first position in ext of v's
+// distance class (pixels of equal dist_from_c are consecutive in ext).  One
+// CTA: per-thread segments, a max-scan of class starts, a block scan of the
+// segment maxima.
+__global__ void __launch_bounds__(1024) k_group_start(const float* dfc, const int* ext, int N, int* gs) {
+  __shared__ int segmax[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int seg = (N + nt - 1) / nt, i0 = min(N, tid * seg), i1 = min(N, i0 + seg);
+  int run = -1;
+  for (int i = i0; i < i1; i++)
+    if (i == 0 || __float_as_uint(dfc[ext[i]]) != __float_as_uint(dfc[ext[i - 1]])) run = i;
+  segmax[tid] = run;
+  __syncthreads();
+  for (int o = 1; o < nt; o <<= 1) {  // inclusive max-scan over the segments
+    const int x = tid >= o ? segmax[tid - o] : -1;
+    __syncthreads();
+    segmax[tid] = max(segmax[tid], x);
+    __syncthreads();
+  }
+  int cur = tid ? segmax[tid - 1] : -1;
+  for (int i = i0; i < i1; i++) {
+    if (i == 0 || __float_as_uint(dfc[ext[i]]) != __float_as_uint(dfc[ext[i - 1]])) cur = i;
+    gs[ext[i]] = cur;
+  }
+}
+
+cudaError_t launch_group_start(const float* dfc, const int* ext, int N, int* gs, cudaStream_t st) {
+  k_group_start<<<1, 1024, 0, st>>>(dfc, ext, N, gs);
+  return cudaGetLastError();
+}
+
 size_t ext_rank_temp_bytes(int N) {
   size_t bytes = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const unsigned long long*)nullptr,

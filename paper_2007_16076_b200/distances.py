@@ -23,6 +23,8 @@ MAX_PIXELS = 10_000
 
 APGD_MAGIC = b"APGD"
 APGD_VERSION = 1
+APGD_VERSION_FLOAT = 2  # additive: fp32 stores (binary64 bits per value)
+APGD_HEADER = len(APGD_MAGIC) + 5
 APGD_SENTINEL = 0xFFFF_FFFF_FFFF_FFFF
 
 #: relative agreement tolerance for float-valued fills (integers: exact)
@@ -140,6 +142,23 @@ class DistanceArray:
         self._filled += new.value
         return new.value
 
+    # ---- one step of a host-selected run (strategies.py:263-271) ----
+    def _set_counts(self, counts: np.ndarray):
+        arr = counts.astype(np.int64)
+        arr.setflags(write=False)
+        self._cache = {"counts": arr}
+
+    def _commit_source(self, graph, source: int, counts: np.ndarray) -> int:
+        """Propagate from `source`, fill its tree (reference checks) and refresh
+        the per-pixel counts: gp_commit_source, one synchronisation."""
+        new = ctypes.c_int64()
+        self._cache.clear()
+        _lib.check(_lib.lib().gp_commit_source(graph.handle, self._st, int(source), self._tol(),
+                                               ctypes.byref(new), _lib.ptr(counts)))
+        self._filled += new.value
+        self._set_counts(counts)
+        return new.value
+
     # ---- host / device views ----
     def _read(self):
         if "D" not in self._cache:
@@ -185,10 +204,99 @@ class DistanceArray:
         self._integer = bool(integer)
         self._cache.clear()
 
+    # ---- APGD dump / load (distances.py:149-177) ----
+    # Row blocks are converted to u64 on the device (gp_store_apgd_rows /
+    # gp_store_load_rows), so no N^2 host temporary is ever built; integer
+    # stores write the reference's version 1, float stores version 2
+    # (additive: binary64 bits of the fp32 value, same sentinel).
+    _TILE_BYTES = 32 << 20
+
+    def _apgd_version(self) -> int:
+        return APGD_VERSION if self._integer else APGD_VERSION_FLOAT
+
+    def _tile_rows(self) -> int:
+        return max(1, self._TILE_BYTES // (8 * self.n))
+
+    def apgd_header(self) -> bytes:
+        return APGD_MAGIC + struct.pack("<BI", self._apgd_version(), self.n)
+
+    def apgd_row_tiles(self):
+        """Yield (row0, u64 array [rows, n]) blocks of the APGD payload."""
+        n, per, ver = self.n, self._tile_rows(), self._apgd_version()
+        buf = np.empty((per, n), dtype="<u8")
+        for r0 in range(0, n, per):
+            k = min(per, n - r0)
+            _lib.check(_lib.lib().gp_store_apgd_rows(self._st, ver, r0, k, _lib.ptr(buf)))
+            yield r0, buf[:k]
+
     def to_bytes(self) -> bytes:
-        """APGD dump (distances.py:149-154)."""
-        D, M = self._read()
-        out = D.astype(np.uint64)
-        out[~M] = APGD_SENTINEL
-        header = APGD_MAGIC + struct.pack("<BI", APGD_VERSION, self.n)
-        return header + out.astype("<u8").tobytes()
+        """Serialize to the APGD binary dump (magic, version, n, u64 grid)."""
+        head = self.apgd_header()
+        out = bytearray(len(head) + 8 * self.n * self.n)
+        out[:len(head)] = head
+        view = np.frombuffer(out, dtype=np.uint8)
+        for r0, blk in self.apgd_row_tiles():
+            o = len(head) + 8 * r0 * self.n
+            view[o:o + blk.nbytes] = blk.reshape(-1).view(np.uint8)
+        return bytes(out)
+
+    def write_apgd(self, f) -> int:
+        """Stream the APGD dump to a binary file object; returns the bytes written."""
+        head = self.apgd_header()
+        f.write(head)
+        total = len(head)
+        for _, blk in self.apgd_row_tiles():
+            f.write(memoryview(np.ascontiguousarray(blk)).cast("B"))
+            total += blk.nbytes
+        return total
+
+    @staticmethod
+    def _apgd_parse_header(head: bytes):
+        if len(head) < APGD_HEADER or head[:4] != APGD_MAGIC:
+            raise ValueError("not an APGD dump (bad magic)")
+        version, n = struct.unpack("<BI", head[4:APGD_HEADER])
+        if version not in (APGD_VERSION, APGD_VERSION_FLOAT):
+            raise ValueError(f"unsupported APGD version {version}")
+        return version, n
+
+    @classmethod
+    def _apgd_store(cls, version: int, n: int, blocks) -> "DistanceArray":
+        store = cls(n, force=True)
+        for r0, blk in blocks:
+            blk = np.ascontiguousarray(blk, dtype="<u8")
+            _lib.check(_lib.lib().gp_store_load_rows(store._st, version, r0, blk.shape[0], _lib.ptr(blk)))
+        filled = ctypes.c_int64()
+        _lib.check(_lib.lib().gp_store_recount(store._st, ctypes.byref(filled)))
+        store._filled = filled.value
+        store._integer = version == APGD_VERSION
+        store._cache.clear()
+        return store
+
+    @classmethod
+    def from_bytes(cls, data: bytes) -> "DistanceArray":
+        """Parse an APGD binary dump back into a DistanceArray."""
+        version, n = cls._apgd_parse_header(bytes(data[:APGD_HEADER]))
+        expected = APGD_HEADER + 8 * n * n
+        if len(data) != expected:
+            raise ValueError(f"APGD dump has {len(data)} bytes, expected {expected}")
+        grid = np.frombuffer(data, dtype="<u8", offset=APGD_HEADER).reshape(n, n)
+        per = max(1, cls._TILE_BYTES // (8 * n))
+        return cls._apgd_store(version, n, ((r0, grid[r0:r0 + per]) for r0 in range(0, n, per)))
+
+    @classmethod
+    def read_apgd(cls, f) -> "DistanceArray":
+        """Stream an APGD dump from a binary file object (no N^2 host buffer)."""
+        version, n = cls._apgd_parse_header(f.read(APGD_HEADER))
+        per = max(1, cls._TILE_BYTES // (8 * n))
+
+        def blocks():
+            for r0 in range(0, n, per):
+                k = min(per, n - r0)
+                raw = f.read(8 * k * n)
+                if len(raw) != 8 * k * n:
+                    raise ValueError("APGD dump is truncated")
+                yield r0, np.frombuffer(raw, dtype="<u8").reshape(k, n)
+            if f.read(1):
+                raise ValueError("APGD dump has trailing bytes")
+
+        return cls._apgd_store(version, n, blocks())

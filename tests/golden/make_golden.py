@@ -9,6 +9,7 @@ exist there):
     python tests/golden/make_golden.py cfg 2      # reference itself (int config)
     python tests/golden/make_golden.py cfg 4      # reference itself, force=True
     python tests/golden/make_golden.py cfg 1|3|5  # fp32 restatement (oracle/)
+    python tests/golden/make_golden.py apgd       # reference: APGD dumps (partial + complete)
     python tests/golden/make_golden.py trees 2    # reference: every source of cfg2
     python tests/golden/make_golden.py trees 4    # reference: 256 sampled + first 64 committed
 
@@ -215,6 +216,34 @@ def make_cfg(index: int, nthreads: int):
     print(f"cfg{index}: raw={raw} adjusted={adjusted} elapsed={elapsed:.1f}s src={source}")
 
 
+def make_apgd():
+    """APGD dumps written by the reference (DistanceArray.to_bytes,
+    distances.py:149-154): a partially filled store (three trees: sentinels)
+    and a complete filling-rate run, per image; the fill sources are recorded."""
+    gp = _ref()
+    rng = np.random.default_rng(2550)
+    out = {}
+    for i, (h, w) in enumerate([(5, 6), (9, 7), (12, 11)]):
+        img = rng.integers(1, 256, (h, w))
+        image = gp.Image(img)
+        graph = gp.GridGraph(image, gp.Metric.SUM)
+        store = gp.DistanceArray(h * w)
+        roots = rng.choice(h * w, 3, replace=False)
+        for r in roots:
+            store.fill_from_tree(gp.build_tree(graph.propagate([int(r)]), int(r)))
+        out[f"c{i}_img"] = img.astype(np.int64)
+        out[f"c{i}_roots"] = roots.astype(np.int64)
+        out[f"c{i}_partial"] = np.frombuffer(store.to_bytes(), dtype=np.uint8)
+        run = gp.run_strategy(image, gp.Metric.SUM, gp.StrategyKind.FILLING_RATE)
+        out[f"c{i}_full"] = np.frombuffer(run.distances.to_bytes(), dtype=np.uint8)
+        back = gp.DistanceArray.from_bytes(store.to_bytes())
+        out[f"c{i}_partial_counts"] = np.array(back.point_filled_counts)
+        out[f"c{i}_partial_filled"] = np.array(back.pairs_filled)
+    out["n_cases"] = np.array(3)
+    np.savez_compressed(os.path.join(HERE, "ref_apgd.npz"), **out)
+    print("apgd cases: 3")
+
+
 def tree_digest(a: np.ndarray) -> np.ndarray:
     """16-byte sha256 prefix of an int64 per-pixel array (dist or parent)."""
     return np.frombuffer(hashlib.sha256(np.ascontiguousarray(a, dtype="<i8").tobytes()).digest()[:16],
@@ -259,6 +288,8 @@ if __name__ == "__main__":
         make_strategies()
     elif sys.argv[1] == "harness":
         make_harness()
+    elif sys.argv[1] == "apgd":
+        make_apgd()
     elif sys.argv[1] == "trees":
         make_trees(int(sys.argv[2]))
     else:

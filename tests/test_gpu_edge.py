@@ -2,6 +2,7 @@
 
 from __future__ import annotations
 
+import hashlib
 import os
 
 import numpy as np
@@ -89,7 +90,8 @@ def test_l1_plateau_run_completes_with_exact_distances(gp, oracle, shape):
     {"GP_SPEC_K": "7"}, {"GP_SPEC_K": "1000"}, {"GP_LIST_ALPHA": "0"}, {"GP_LIST_ALPHA": "1000"},
     {"GP_UNITS_PER_WARP": "4"}, {"GP_DELTA_FACTOR": "inf"}, {"GP_DELTA_FACTOR": "0.5"},
     {"GP_PROP_THREADS": "256"}, {"GP_BARRIER": "sw"}, {"GP_PIPELINE": "0"}, {"GP_FILL_QUEUE": "0"},
-    {"GP_FILL_UNROLL": "1"}, {"GP_FILL_UNROLL": "8"}, {"GP_OVERLAP": "1"}, {"GP_PROP_MINB": "2"},
+    {"GP_FILL_UNROLL": "1"}, {"GP_FILL_UNROLL": "8"}, {"GP_PROP_MINB": "2"},
+    {"GP_PROP_CLUSTER": "2"}, {"GP_PROP_CLUSTER": "2", "GP_LIST_ALPHA": "1000"}, {"GP_VERIFY": "1"},
     {"GP_CAND": "0"}, {"GP_LPT": "0"}, {"GP_COMMIT_SPLIT": "0"}, {"GP_LIST_CFG": "2"}, {"GP_LIST_CFG": "1"}, {"GP_PROP_LEAN": "0"}, {"GP_PROP_MC": "0"},
     {"GP_COMPACT_DIV": "1"}, {"GP_COMPACT_DIV": "64"}, {"GP_LIST_ALPHA": "1", "GP_COMPACT_DIV": "1"},
 ])
@@ -266,3 +268,40 @@ def test_max_size_runs_rows_equal_propagations(gp, oracle, shape, conn, isint):
             assert np.array_equal(row, np.asarray(d, dtype=np.float32)), s
         else:
             assert np.allclose(row, d, rtol=1e-4, atol=1e-6), s
+
+
+@pytest.mark.parametrize("shape,conn", [((7, 9), 8), ((9, 7), 4), ((1, 13), 8), ((16, 17), 8), ((33, 30), 4)])
+@pytest.mark.parametrize("isint", [True, False])
+def test_cluster_propagation_small_maps_match_oracle(gp, oracle, monkeypatch, shape, conn, isint):
+    """The 2-CTA cluster K1 (GP_PROP_CLUSTER=2 forces it on maps that fit one
+    SM) against the oracle: odd pixel counts, single rows, 4/8-connectivity."""
+    rng = np.random.default_rng(shape[0] * 100 + shape[1] + conn)
+    img = rng.integers(1, 256, shape) if isint else rng.random(shape, dtype=np.float32)
+    monkeypatch.setenv("GP_PROP_CLUSTER", "2")
+    for kind, k in (("filling-rate", gp.StrategyKind.FILLING_RATE), ("naive", gp.StrategyKind.NAIVE)):
+        o = oracle.run(img, kind, conn=conn, naive_with_tree=kind == "naive")
+        run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, k, connectivity=conn,
+                              naive_with_tree=kind == "naive")
+        assert _seq(run) == o["seq"].tolist()
+        assert np.array_equal(run.distances.dist, o["D"])
+
+
+@pytest.mark.parametrize("shape,conn,metric,isint", [
+    ((140, 130), 8, "sum", False), ((131, 160), 4, "mean", True), ((133, 137), 8, "sum", True),
+])
+def test_cluster_and_single_cta_k1_runs_identical(gp, monkeypatch, shape, conn, metric, isint):
+    """Maps above one SM's shared memory: the cluster K1 (default) and the
+    single-CTA global-scratch K1 (GP_PROP_CLUSTER=0) give the same run --
+    source sequence, new pairs per commit, and the whole distance array."""
+    rng = np.random.default_rng(sum(shape))
+    img = rng.integers(1, 256, shape) if isint else rng.random(shape, dtype=np.float32)
+    m = {"sum": gp.Metric.SUM, "mean": gp.Metric.MEAN}[metric]
+    out = []
+    for knob in ("1", "0"):
+        monkeypatch.setenv("GP_PROP_CLUSTER", knob)
+        run = gp.run_strategy(gp.Image(img), m, gp.StrategyKind.FILLING_RATE, connectivity=conn, force=True)
+        Dd = run.distances.dist_device()
+        h = hashlib.sha256(Dd.cpu().numpy().tobytes()).hexdigest()
+        out.append(([s for _, s, _ in run.trace.samples], [f for _, _, f in run.trace.samples], h))
+        del run, Dd
+    assert out[0] == out[1]
