@@ -22,8 +22,9 @@ see DESIGN.md), value = N * A * K / max-over-ranks(device time of K steps).
   divided by the summed k_commit event time.
 * cpu_baseline (rank 0, N=1): the oracle port (oracle/, C; the reference
   rejects fp32 images) on 1 host core -- the reference is single-threaded --
-  over the first M commits of the run, whole image extrapolated as per-commit
-  time x P (labelled); the port on all host threads beside it; the UNMODIFIED
+  over two prefixes of the run, whole image extrapolated from the marginal
+  segment in proportion to ancestor visits (labelled; conservative); the port
+  on all host threads beside it; the UNMODIFIED
   reference (baseline/_ref, numba) on the integer configs: cfg2 whole image
   measured, cfg4 a replayed prefix of the committed sequence, extrapolated.
 * --impl reference: the oracle port with all host threads, bounded prefix per
@@ -134,10 +135,10 @@ def _traffic(config: int, kernel: str):
 
 
 def _golden_counts(index: int):
-    """P (raw, adjusted) of the committed sequence from the committed golden
-    fixture (equal to the GPU run's by the parity tests)."""
+    """P (raw, adjusted) and the visits C of the committed sequence from the
+    committed golden fixture (equal to the GPU run's by the parity tests)."""
     g = np.load(os.path.join(ROOT, "tests", "golden", f"cfg{index}.npz"))
-    return int(g["raw"]), int(g["adjusted"])
+    return int(g["raw"]), int(g["adjusted"]), int(g["visits"].sum())
 
 
 def _config_dict(spec, P: int, P_adj: int, world: int) -> dict:
@@ -148,32 +149,47 @@ def _config_dict(spec, P: int, P_adj: int, world: int) -> dict:
             "l2": "flushed (256 MiB write) between steps"}
 
 
-def _port_sample(img, spec, P: int, target_s: float, nthreads: int):
-    """The oracle port's real loop (selection + propagation + tree fill) for
-    the first M commits of the run, timed inside the loop (allocation
-    excluded); the whole image is extrapolated as per-commit time x P (the
-    fill of every commit walks all ancestor pairs of its tree, reference
-    _kernels.py:96-115, so the per-commit cost is flat over the run)."""
+def _port_sample(img, spec, P: int, C: int, target_s: float, nthreads: int, m2: int = 0):
+    """The oracle port's real loop (selection + propagation + tree fill) over
+    two prefixes of the run (M1 < M2 commits, timed inside the loop,
+    allocation excluded).  The whole image is extrapolated from the marginal
+    segment M1..M2 (first-touch effects of the first commits excluded) in
+    proportion to ancestor visits: t_image = (t2 - t1) * C / (C2 - C1), C =
+    the run's visits (sum of tree depths).  The fill walks every ancestor pair
+    of each tree (reference _kernels.py:96-115) and visits per commit decline
+    over the run, so this undercounts the per-commit propagation cost of late
+    commits: a conservative (low) CPU time."""
     from oracle import oracle as O
 
-    m = min(spec.n, 4)
-    r = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m)
-    per = r["loop_seconds"] / max(r["raw"], 1)
-    m = int(min(spec.n, max(m, target_s / max(per, 1e-6))))
-    r = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m)
-    dt, pairs, k = r["loop_seconds"], r["filled"], int(r["raw"])
-    per = dt / max(k, 1)
-    ms_image = per * P * 1e3
+    m1 = min(spec.n, 32)
+    t0 = 0.0
+    if not m2:  # calibration: marginal per-commit time beyond the first touches
+        m0 = min(spec.n, 8)
+        t0 = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m0)["loop_seconds"]
+    r1 = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m1)
+    if not m2:
+        per = (r1["loop_seconds"] - t0) / max(m1 - m0, 1)
+        m2 = int(min(spec.n, m1 + max(m1, 0.6 * target_s / max(per, 1e-6))))
+    r2 = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m2)
+    t1, t2 = r1["loop_seconds"], r2["loop_seconds"]
+    c1, c2 = int(r1["visits"].sum()), int(r2["visits"].sum())
+    k1, k2 = int(r1["raw"]), int(r2["raw"])
+    per_visit = (t2 - t1) / max(c2 - c1, 1)
+    ms_image = per_visit * C * 1e3
     return {
         "value": spec.total_pairs / (ms_image / 1e3), "unit": "pairs/s", "cores": nthreads,
         "cores_available": os.cpu_count(), "kind": "port",
-        "ms_per_image": ms_image, "ms_per_image_kind": f"extrapolated: per-commit time of the first {k} commits x P={P}",
-        "per_commit_ms": per * 1e3, "commits_timed": k, "seconds": dt,
-        "prefix_pairs_per_s": pairs / dt,
+        "ms_per_image": ms_image,
+        "ms_per_image_kind": (f"extrapolated: marginal time of commits {k1}..{k2} per ancestor visit x the run's "
+                              f"C={C} visits (P={P} commits)"),
+        "per_commit_ms": (t2 - t1) / max(k2 - k1, 1) * 1e3, "commits_timed": k2,
+        "seconds": t0 + t1 + t2, "m2": k2,
+        "prefix_pairs_per_s": r2["filled"] / t2,
         "sample": (f"oracle/oracle.c (C restatement of the reference loop; the reference rejects fp32 images) "
-                   f"on {nthreads} of {os.cpu_count()} host threads: the first {k} commits of the "
-                   f"{spec.name} filling-rate run in {dt:.2f}s ({per * 1e3:.1f} ms per commit), whole image "
-                   f"extrapolated to {ms_image / 1e3:.0f}s for P={P} commits"),
+                   f"on {nthreads} of {os.cpu_count()} host threads: the first {k1} and {k2} commits of the "
+                   f"{spec.name} filling-rate run in {t1:.2f}s / {t2:.2f}s; commits {k1}..{k2} took "
+                   f"{(t2 - t1) / max(k2 - k1, 1) * 1e3:.1f} ms each ({(c2 - c1) / max(k2 - k1, 1) / 1e6:.1f} M "
+                   f"visits each); whole image extrapolated by visits to {ms_image / 1e3:.0f}s"),
     }
 
 
@@ -195,14 +211,14 @@ def _ref_timing(mode: str, index: int, extra=None, timeout: float = 900.0):
         return {"unavailable": f"reference timing failed: {type(e).__name__}: {e}"[:300]}
 
 
-def cpu_baseline(img, spec, index: int, P: int, target_s: float):
+def cpu_baseline(img, spec, index: int, P: int, C: int, target_s: float):
     """cpu_baseline of the headline line (rank 0, N=1): the oracle port on 1
     host core (the reference is single-threaded) with the whole image
     extrapolated, the port on all host threads beside it, and the reference
     itself on the integer configs (cfg2 whole image measured, cfg4 a replayed
     prefix of the committed sequence, extrapolated)."""
-    one = _port_sample(img, spec, P, target_s, 1)
-    allt = _port_sample(img, spec, P, target_s, os.cpu_count() or 1)
+    one = _port_sample(img, spec, P, C, target_s, 1)
+    allt = _port_sample(img, spec, P, C, target_s, os.cpu_count() or 1)
     one["port_all_threads"] = {k: allt[k] for k in ("value", "cores", "ms_per_image", "per_commit_ms",
                                                      "commits_timed", "seconds", "prefix_pairs_per_s")}
     one["reference_cfg2"] = _ref_timing("full", 2)
@@ -214,22 +230,28 @@ def run_reference(args, spec, img, world, rank):
     """--impl reference: the reference path's CPU implementation on the host
     cores -- the oracle port (the reference itself rejects the fp32 headline
     image) with all host threads; each step a bounded prefix of the run, the
-    whole image extrapolated (per-commit time x P)."""
+    whole image extrapolated the same way (marginal time per visit x C)."""
     if rank != 0:
         return
     nthreads = os.cpu_count() or 1
-    P, P_adj = _golden_counts(args.config)
+    P, P_adj, C = _golden_counts(args.config)
     vals, samples = [], []
+    budget = max(3.0, min(args.cpu_seconds, 180.0 / (args.warmup + args.steps)))  # seconds per step
+    m2 = 0
     for i in range(args.warmup + args.steps):
-        r = _port_sample(img, spec, P, args.cpu_seconds, nthreads)
+        r = _port_sample(img, spec, P, C, budget, nthreads, m2)
+        m2 = r["m2"]
         if i >= args.warmup:
             vals.append(r["value"])
             samples.append(r)
     v = statistics.mean(vals)
-    ms = statistics.mean(s["ms_per_image"] for s in samples)
+    ms = statistics.mean(s["seconds"] for s in samples) * 1e3  # measured time of a step's bounded sample
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "value_kind": ("whole-image pairs/s extrapolated from each step's bounded sample (cpu_baseline."
+                       "ms_per_image_kind); ms_per_step is the measured time of one step's sample"),
+        "ms_per_image_extrapolated": statistics.mean(s["ms_per_image"] for s in samples),
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if spec.dtype == "f32" else "f32 (integer-exact)",
         "data": "synthetic (seeded generator, paper_2007_16076_b200/configs.py)",
@@ -258,15 +280,18 @@ def aggregate(total_ms: float, pairs_per_image: int, steps: int, world: int, dis
 
 
 def _other_configs(L, _lib, skip: int):
-    """One device-timed run of every other BASELINE config (not the headline)."""
+    """One device-timed run of every other BASELINE config (not the headline),
+    plus the extrema strategy (device K3 key variant) on
+    the config-4 image."""
     out = {}
-    for idx, spec in CONFIGS.items():
-        if idx == skip:
-            continue
+    runs = [(idx, spec, spec.strategy, spec.name) for idx, spec in CONFIGS.items() if idx != skip]
+    runs.append((4, CONFIGS[4], "extrema", "cfg4_image_extrema_8c"))
+    for idx, spec, strategy, name in runs:
         img = make_image(idx)
         px = np.ascontiguousarray(img.astype(np.float32) if spec.dtype == "f32" else img)
         dtype = _lib.DTYPE_F32 if spec.dtype == "f32" else _lib.DTYPE_U8
-        strat = _lib.STRATEGY_FILLING_RATE if spec.strategy == "filling-rate" else _lib.STRATEGY_NAIVE
+        strat = {"filling-rate": _lib.STRATEGY_FILLING_RATE, "naive": _lib.STRATEGY_NAIVE,
+                 "extrema": _lib.STRATEGY_EXTREMA}[strategy]
         h, st = ctypes.c_void_p(), ctypes.c_void_p()
         _lib.check(L.gp_ctx_create(spec.shape[0], spec.shape[1], dtype, _lib.ptr(px), 1, spec.conn,
                                    ctypes.byref(h)))
@@ -276,7 +301,7 @@ def _other_configs(L, _lib, skip: int):
             s = _lib.RunStats()
             _lib.check(L.gp_run(h, st, strat, 0, 0, None, None, ctypes.byref(s)))
             best = s
-        out[spec.name] = {"ms_per_image": best.ms_total, "pairs_per_s": spec.total_pairs / (best.ms_total / 1e3),
+        out[name] = {"ms_per_image": best.ms_total, "pairs_per_s": spec.total_pairs / (best.ms_total / 1e3),
                           "propagations_raw": int(best.raw_count), "ms_commit": best.ms_commit,
                           "ms_propagate": best.ms_propagate}
         L.gp_store_destroy(st)
@@ -292,7 +317,7 @@ def main():
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=16.0)
     ap.add_argument("--no-others", action="store_true", help="skip the one-run summary of the other configs")
     args = ap.parse_args()
     world, rank, local = _dist_env()
@@ -419,7 +444,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_others:
         line["other_configs"] = _other_configs(L, _lib, args.config)
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(img, spec, args.config, P, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(img, spec, args.config, P, C, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
     L.gp_store_destroy(st)

@@ -334,6 +334,11 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
 #define GP_FQ_CAP 4096
 #endif
 constexpr int FQ_CAP = GP_FQ_CAP;
+// phase-A schedule anchors (see the comment in fill_tree_cta): 0 = the debug
+// stamps (default), 1 = empty asm memory fences, 2 = none (measured slower)
+#ifndef GP_PHASEA_ANCHOR
+#define GP_PHASEA_ANCHOR 0
+#endif
 struct FillQ {
   uint2 desc[FQ_CAP];
   int n, res, head;
@@ -474,7 +479,11 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
         if (cn4[i]) lnew += fill_unit<(G > 4 ? 4 : G)>(a, slot, s, (int)blockIdx.x + (k0 + i * nw) * NB);
       continue;
     }
+#if GP_PHASEA_ANCHOR == 0
     if (stamp) sim[4] = gtimer() - t_a0 + (unsigned long long)(q4[0] + q4[1] + q4[2] + q4[3]) * 0ull;
+#elif GP_PHASEA_ANCHOR == 1
+    asm volatile("" ::"r"(q4[0]), "r"(q4[1]), "r"(q4[2]), "r"(q4[3]) : "memory");
+#endif
     unsigned my4[4], c04[4], tk4[4];
     int cv4[4];
 #pragma unroll
@@ -483,7 +492,11 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
       const int u_l = (int)(e4[i] & 0xFFFFu);
       cv4[i] = (my4[i] && u_l != s) ? __ldcg(&a.cnt[u_l]) : 0;
     }
+#if GP_PHASEA_ANCHOR == 0
     if (stamp) sim[5] = gtimer() - t_a0 + (unsigned long long)(tk4[0] + tk4[3]) * 0ull;
+#elif GP_PHASEA_ANCHOR == 1
+    asm volatile("" ::"r"(tk4[0]), "r"(tk4[3]) : "memory");
+#endif
     // first windows of the four units: one reservation, independent chains
     unsigned nop4[4], inc4[4], wt4[4], wsum = 0;
 #pragma unroll
@@ -499,7 +512,11 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
       fq_write(Q, lane, (unsigned)base, wt4[i], inc4[i], nop4[i], (int)q4[i], e4[i], sz4[i], c04[i]);
       base += (int)wt4[i];
     }
+#if GP_PHASEA_ANCHOR == 0
     if (stamp) sim[6] = gtimer() - t_a0;
+#elif GP_PHASEA_ANCHOR == 1
+    asm volatile("" ::: "memory");
+#endif
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       unsigned count = cn4[i] - tk4[i];

@@ -10,6 +10,7 @@ exist there):
     python tests/golden/make_golden.py cfg 4      # reference itself, force=True
     python tests/golden/make_golden.py cfg 1|3|5  # fp32 restatement (oracle/)
     python tests/golden/make_golden.py apgd       # reference: APGD dumps (partial + complete)
+    python tests/golden/make_golden.py extrema 2  # reference: EXTREMA strategy on the cfg2 image
     python tests/golden/make_golden.py trees 2    # reference: every source of cfg2
     python tests/golden/make_golden.py trees 4    # reference: 256 sampled + first 64 committed
 
@@ -216,6 +217,27 @@ def make_cfg(index: int, nthreads: int):
     print(f"cfg{index}: raw={raw} adjusted={adjusted} elapsed={elapsed:.1f}s src={source}")
 
 
+def make_extrema(index: int):
+    """The reference's EXTREMA strategy (strategies.py:195-210) on an integer
+    config image: sequence, per-commit new pairs, counts and a digest of D."""
+    gp = _ref()
+    spec = CONFIGS[index]
+    image = gp.Image(make_image(index).astype(np.int64))
+    t0 = time.time()
+    run = gp.run_strategy(image, gp.Metric.SUM, gp.StrategyKind.EXTREMA, force=True)
+    elapsed = time.time() - t0
+    A = spec.total_pairs
+    filled = np.array([int(tau * A) for _, _, tau in run.trace.samples], dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, f"extrema{index}.npz"),
+                        seq=np.array([s for _, s, _ in run.trace.samples], dtype=np.int32),
+                        new=np.diff(np.concatenate([[0], filled])), raw=np.array(run.trace.raw_count),
+                        adjusted=np.array(run.trace.adjusted_count),
+                        d_sha256=np.array(d_digest(run.distances.dist, False)),
+                        source=np.array("reference geopairs run_strategy(EXTREMA)"),
+                        cpu_seconds=np.array(elapsed))
+    print(f"extrema{index}: raw={run.trace.raw_count} elapsed={elapsed:.1f}s")
+
+
 def make_apgd():
     """APGD dumps written by the reference (DistanceArray.to_bytes,
     distances.py:149-154): a partially filled store (three trees: sentinels)
@@ -288,6 +310,8 @@ if __name__ == "__main__":
         make_strategies()
     elif sys.argv[1] == "harness":
         make_harness()
+    elif sys.argv[1] == "extrema":
+        make_extrema(int(sys.argv[2]))
     elif sys.argv[1] == "apgd":
         make_apgd()
     elif sys.argv[1] == "trees":

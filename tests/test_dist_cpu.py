@@ -66,3 +66,16 @@ def test_committed_traffic_evidence_feeds_roofline():
     assert k["launches"] > 0 and k["dram_bytes"] > 0
     assert abs(k["dram_bytes_per_launch"] * k["launches"] - k["dram_bytes"]) < 1e-6 * k["dram_bytes"]
     assert bench._traffic(999, "k_commit") == (None, None)
+
+
+def test_both_arms_share_the_config_dict():
+    """--impl reference builds its `config` with the same function and the same
+    (golden) propagation counts as the repo arm, so the driver sees one config."""
+    import bench
+    from paper_2007_16076_b200.configs import CONFIGS
+
+    P, P_adj, C = bench._golden_counts(5)
+    assert (P, P_adj) == (52191, 52193) and C == 423501991006
+    a = bench._config_dict(CONFIGS[5], P, P_adj, 1)
+    assert a == bench._config_dict(CONFIGS[5], 52191, 52193, 1)
+    assert a["workload"] == CONFIGS[5].name and a["pairs_per_image"] == CONFIGS[5].total_pairs

@@ -235,3 +235,25 @@ def test_spec_k_above_topk_capacity(gp):
     big = gp.run_strategy(gp.Image(img), gp.Metric.SUM, gp.StrategyKind.FILLING_RATE, spec_k=2048)
     assert [s for _, s, _ in big.trace.samples] == [s for _, s, _ in base.trace.samples]
     assert np.array_equal(big.distances.dist, base.distances.dist)
+
+
+def test_extrema_and_small_entry_points(gp, ref_small):
+    """gp_extrema (compute_extrema_context, strategies.py:104-116) against the
+    reference's centroid / dist_from_c / ext; gp_ctx_num_pixels; counts."""
+    from conftest import small_cases
+    from paper_2007_16076_b200 import _lib
+
+    for i, c in small_cases(ref_small):
+        img, metric = c["img"], str(c["metric"])
+        m = {"sum": gp.Metric.SUM, "mean": gp.Metric.MEAN, "l1": gp.Metric.L1}[metric]
+        ctx = gp.compute_extrema_context(gp.Image(img), m)
+        assert ctx.centroid == int(c["centroid"]), i
+        assert np.array_equal(np.asarray(ctx.dist_from_c), c["dfc"]), i
+        assert np.array_equal(np.asarray(ctx.ext), c["ext"]), i
+        graph = gp.GridGraph(gp.Image(img), m)
+        assert _lib.lib().gp_ctx_num_pixels(graph.handle) == img.size
+    store = gp.DistanceArray(9)
+    counts = np.empty(9, np.int32)
+    filled = ctypes.c_int64()
+    _lib.check(_lib.lib().gp_store_counts(store._st, _lib.ptr(counts), ctypes.byref(filled)))
+    assert counts.tolist() == [0] * 9 and filled.value == 0

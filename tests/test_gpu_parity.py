@@ -212,3 +212,16 @@ def test_other_strategies_match_reference(gp):
             assert run.trace.adjusted_count == int(g[k + tag + "_adj"]), (i, tag)
             rates = [Fraction(int(a), int(b)) for a, b in g[k + tag + "_rates"]]
             assert [f for _, _, f in run.trace.samples] == rates, (i, tag)
+
+
+def test_extrema_config2_matches_reference(gp):
+    """The device extrema selector (K3 key variant) against the reference's
+    own EXTREMA run on the config-2 image (tests/golden/extrema2.npz)."""
+    g = load_golden("extrema2.npz")
+    spec = CONFIGS[2]
+    run = gp.run_strategy(gp.Image(make_image(2)), gp.Metric.SUM, gp.StrategyKind.EXTREMA)
+    assert [s for _, s, _ in run.trace.samples] == g["seq"].tolist()
+    filled = np.array([int(f * spec.total_pairs) for _, _, f in run.trace.samples], dtype=np.int64)
+    assert np.array_equal(np.diff(np.concatenate([[0], filled])), g["new"])
+    assert run.trace.adjusted_count == int(g["adjusted"])
+    assert _digest(run.distances.dist_device().cpu().numpy(), False) == str(g["d_sha256"])
