@@ -52,6 +52,8 @@ struct gp_ctx {
   int commit_blocks = 0;
   double mean_w = 1.0;  // mean edge weight (bucket width scale)
   int pos_w = 0;        // every edge weight > 0
+  unsigned long long* heap = nullptr;  // exact heap-order K1 scratch (images with zero-weight edges)
+  size_t heap_trees = 0;
   uint32_t* list[2] = {nullptr, nullptr};  // unfilled-pair lists (late phase)
   int* h_cnt2 = nullptr;     // pinned: two count snapshots (host-row rounds)
   Ctl* h_ctl2 = nullptr;     // pinned: two control-block snapshots
@@ -213,6 +215,7 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
   for (void* p : c->ws) cudaFree(p);
   cudaFree(c->bar);
   cudaFree(c->scratch);
+  cudaFree(c->heap);
   if (c->st) cudaStreamDestroy(c->st);
   if (c->st2) cudaStreamDestroy(c->st2);
   if (c->st3) cudaStreamDestroy(c->st3);
@@ -243,7 +246,24 @@ static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
   return cudaSuccess;
 }
 
+// Heap scratch of the exact heap-order K1 (zero-weight edges only): at most
+// 2 GiB; larger launches are chunked to what it holds.
+static int ensure_heap(gp_ctx* c, size_t ntrees) {
+  if (c->pos_w) return GP_OK;
+  const size_t words = prop_heap_words(c->g.N, c->g.N);
+  const size_t cap = std::max<size_t>(1, ((size_t)2 << 30) / (words * 8));
+  const size_t want = std::min(ntrees, cap);
+  if (want <= c->heap_trees) return GP_OK;
+  cudaFree(c->heap);
+  c->heap = nullptr;
+  c->heap_trees = 0;
+  CUDA_TRY(dalloc(&c->heap, words * want));
+  c->heap_trees = want;
+  return GP_OK;
+}
+
 static int ensure_scratch(gp_ctx* c, size_t ntrees) {
+  if (int rc = ensure_heap(c, ntrees)) return rc;
   if (ntrees <= c->scratch_trees) return GP_OK;
   // single-CTA global-scratch K1, or the overflow lists of the cluster K1
   const size_t per = prop_fits_smem(c->g.N) ? prop_cluster_scratch(c->g.N)
@@ -264,6 +284,10 @@ static PropArgs base_prop(gp_ctx* c) {
   a.scratch = c->scratch;
   a.delta = INFINITY;
   a.pos_weights = c->pos_w;
+  a.exact_heap = c->pos_w ? 0 : 1;
+  a.heap = c->heap;
+  a.heap_words = prop_heap_words(c->g.N, c->g.N);
+  a.heap_trees = (int)c->heap_trees;
   return a;
 }
 

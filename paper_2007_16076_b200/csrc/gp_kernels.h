@@ -53,7 +53,14 @@ struct PropArgs {
   const int* list_mode;    // optional &Ctl::mode: == 1 -> list-mode tree (tin/tdp/C only)
   int pos_weights;         // every edge weight > 0 (closed-form parents; cluster K1 allowed)
   unsigned long long* cl_dbg;  // optional cluster-K1 phase time sums [16] (GP_CL_DEBUG)
+  int tree_base;           // index of the launch's first tree (chunked launches)
+  int exact_heap;          // zero-weight edges: sequential heap-order Dijkstra (generic K1)
+  unsigned long long* heap;  // per-CTA heap scratch [heap_words] (exact_heap)
+  size_t heap_words;         // u64 words per CTA: heap (8N + ns + 1) + parent codes (N bytes)
+  int heap_trees;            // CTAs the heap scratch holds (launches are chunked to it)
 };
+// heap scratch words of one tree (exact_heap): heap (8N + ns + 1 keys) + N code bytes
+inline size_t prop_heap_words(int N, int ns) { return 8 * (size_t)N + (size_t)ns + 1 + ((size_t)N + 7) / 8; }
 
 size_t prop_smem_bytes(int N);
 size_t prop_scratch_bytes(int N);

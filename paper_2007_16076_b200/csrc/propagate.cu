@@ -198,6 +198,72 @@ __device__ void pointer_jump_global(uint32_t* pj, int N) {
   }
 }
 
+// Exact restatement of dijkstra_csr (_kernels.py:33-79) for images with
+// zero-weight edges (L1 metric on equal neighbours; zero pixels), run by one
+// thread of the tree's CTA: a binary heap keyed by (dist, id) -- the
+// reference's dist * n + id order; keys are unique, so any correct min-heap
+// pops in the reference's order --, stale entries skipped, the parent set on
+// strict improvement only.  Without zero-weight edges the closed-form rule of
+// the post-pass reproduces that order; on a zero-weight plateau
+// the pops within one distance level follow the heap's discovery order,
+// which only this sequential simulation gives.  Writes dist (fp32 bits) and
+// the parent window codes (GP_ROOT for sources).
+__device__ void heap_dijkstra(const Grid& g, int metric, int conn, const float* f, volatile uint32_t* dist,
+                              const int* src, int ns, unsigned long long* heap, uint8_t* pcode) {
+  const int N = g.N;
+  for (int v = 0; v < N; v++) pcode[v] = GP_ROOT;
+  int size = 0;
+  auto push = [&](unsigned long long key) {
+    int j = size++;
+    heap[j] = key;
+    while (j > 0) {
+      const int up = (j - 1) >> 1;
+      const unsigned long long hu = heap[up];
+      if (hu <= key) break;
+      heap[j] = hu;
+      j = up;
+    }
+    heap[j] = key;
+  };
+  for (int i = 0; i < ns; i++) push((unsigned long long)(unsigned)src[i]);  // dist 0
+  while (size > 0) {
+    const unsigned long long key = heap[0];
+    const unsigned long long last = heap[--size];
+    int j = 0;
+    for (;;) {  // sift the last entry down from the root
+      const int l = 2 * j + 1, r = l + 1;
+      if (l >= size) break;
+      int m = l;
+      unsigned long long hm = heap[l];
+      if (r < size) {
+        const unsigned long long hr = heap[r];
+        if (hr < hm) { m = r; hm = hr; }
+      }
+      if (hm >= last) break;
+      heap[j] = hm;
+      j = m;
+    }
+    if (size > 0) heap[j] = last;
+    const int u = (int)(key & 0xFFFFFFFFull);
+    const uint32_t db = (uint32_t)(key >> 32);
+    if (db != dist[u]) continue;  // stale entry
+    int r, c;
+    pix_rc(g, u, r, c);
+    const float d = __uint_as_float(db), fu = f[u];
+    for (int k = 0; k < 9; k++) {  // ascending neighbour id = the CSR row order
+      if (!k_in_conn(conn, k)) continue;
+      const int v = nbr_at(g, r, c, k);
+      if (v < 0) continue;
+      const uint32_t nb = __float_as_uint(__fadd_rn(d, edge_w(metric, fu, f[v])));
+      if (nb < dist[v]) {
+        dist[v] = nb;
+        pcode[v] = (uint8_t)(8 - k);  // u relative to v
+        push(((unsigned long long)nb << 32) | (unsigned)v);
+      }
+    }
+  }
+}
+
 // VAR: 0 = generic (variant, outputs and debug stamps decided at run time);
 // 1 / 2 = lean global-scratch / shared-memory variant for speculative
 // batches: Euler-tour outputs only, no naive epilogue, no API outputs, no
@@ -211,17 +277,18 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   const Grid g = a.g;
   const int gmetric = MC ? (int)kSum : g.metric, gconn = MC ? 8 : g.conn;
   const int N = g.N, NW = (N + 31) >> 5;
-  const int t = blockIdx.x;
+  const int t = a.tree_base + (int)blockIdx.x;  // tree index (chunked launches: base + CTA)
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5;
   if (a.ntrees_dev && t >= *a.ntrees_dev) return;
+  const bool exact = !LEAN && a.exact_heap;  // zero-weight edges: sequential heap order
   __shared__ PropShared sh;
   unsigned long long* dbg = (!LEAN && a.dbg) ? a.dbg + (size_t)t * 16 : nullptr;
   if (dbg && tid == 0) { dbg[0] = gtimer(); dbg[12] = 0; dbg[13] = 0; }
 
   const size_t hist_cap = in_smem ? HIST_SMEM : HIST_G;
   const Layout lay = prop_layout(N, hist_cap);
-  unsigned char* base = in_smem ? g_smem : a.scratch + (size_t)t * a.scratch_bytes;
+  unsigned char* base = in_smem ? g_smem : a.scratch + (size_t)blockIdx.x * a.scratch_bytes;
   uint32_t* dist = reinterpret_cast<uint32_t*>(base);
   float* fimg = reinterpret_cast<float*>(base + lay.A);
   WorkLists wl;
@@ -278,7 +345,13 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   float thr = a.delta;
   int cur = 0;
   unsigned passes = 0, items_total = 0;
-  for (;;) {
+  unsigned long long* hp = exact ? a.heap + (size_t)blockIdx.x * a.heap_words : nullptr;
+  uint8_t* pcode = exact ? reinterpret_cast<uint8_t*>(hp + (8 * (size_t)N + a.ns + 1)) : nullptr;
+  if (exact) {
+    if (tid == 0) heap_dijkstra(g, gmetric, gconn, f, vdist, my_src, a.ns, hp, pcode);
+    __syncthreads();
+  }
+  for (; !exact;) {
     int n = sh.cnt[cur];
     if (n == 0) {
       const unsigned long long ta0 = dbg ? gtimer() : 0ull;
@@ -503,7 +576,9 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   for (int v = tid; v < N; v += nthr) {
     uint8_t cv = GP_ROOT;
     const uint32_t dvb = in_smem ? vdist[v] : __ldcg(&dist[v]);
-    if (!((vfar[v >> 5] >> (v & 31)) & 1u)) {
+    if (exact) {
+      cv = *(volatile uint8_t*)&pcode[v];
+    } else if (!((vfar[v >> 5] >> (v & 31)) & 1u)) {
       const float dv = __uint_as_float(dvb);
       int r, c;
       pix_rc(g, v, r, c);
@@ -1032,9 +1107,14 @@ static const void* prop_kernel(const PropArgs& a, int N, int threads) {
   const size_t per_cta = prop_dyn_smem(N) + 1024 + sizeof(PropShared);
   int minb = 3;
   if (const char* e = getenv("GP_PROP_MINB")) minb = atoi(e);
-  const bool lean = !a.dbg && !a.D && !a.out_dist && !a.out_dir && a.ts.pre &&
+  const bool lean = !a.dbg && !a.D && !a.out_dist && !a.out_dir && a.ts.pre && !a.exact_heap &&
                     !(getenv("GP_PROP_LEAN") && !atoi(getenv("GP_PROP_LEAN")));
   const bool mc = a.g.metric == kSum && a.g.conn == 8 && !(getenv("GP_PROP_MC") && !atoi(getenv("GP_PROP_MC")));
+  // experimental CTA shapes of the lean global-scratch K1 (GP_PROP_THREADS /
+  // GP_PROP_MINB): 768 x 2 and 384 x 4 trees per SM
+  if (!prop_fits_smem(N) && lean && mc && threads == 768 && minb == 2) return (const void*)k_propagate<768, 2, 1, 1>;
+  if (!prop_fits_smem(N) && lean && mc && threads == 384 && minb == 4 && (228 * 1024) / per_cta >= 4)
+    return (const void*)k_propagate<384, 4, 1, 1>;
   if (!prop_fits_smem(N) && threads == 512 && minb == 3 && (228 * 1024) / per_cta >= 3) {
     if (lean) return mc ? (const void*)k_propagate<512, 3, 1, 1> : (const void*)k_propagate<512, 3, 1>;
     return (const void*)k_propagate<512, 3>;
@@ -1080,6 +1160,16 @@ static bool use_cluster(const PropArgs& a) {
 
 cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st) {
   if (ntrees <= 0) return cudaSuccess;
+  if (a.exact_heap && a.heap_trees > 0 && ntrees > a.heap_trees) {
+    // the heap scratch holds heap_trees trees: launch in chunks of that many
+    for (int t0 = 0; t0 < ntrees; t0 += a.heap_trees) {
+      PropArgs b = a;
+      b.tree_base = a.tree_base + t0;
+      cudaError_t e = launch_propagate(b, std::min(a.heap_trees, ntrees - t0), st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   if (use_cluster(a)) return launch_propagate_cluster(a, ntrees, st);
   a.in_smem = prop_fits_smem(a.g.N) ? 1 : 0;
   if (!a.in_smem) a.scratch_bytes = prop_scratch_bytes(a.g.N);

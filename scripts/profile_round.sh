@@ -4,7 +4,7 @@
 # Every ncu command runs only after the same program exited 0 without ncu.
 # Outputs land in gpurun_out/<tag>_*; summaries are copied into profiles/ by hand.
 set -u
-TAG=${1:-r01}
+TAG=${1:-r02}
 CFG=${2:-5}
 O=gpurun_out
 mkdir -p $O

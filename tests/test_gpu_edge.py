@@ -62,10 +62,11 @@ def test_l1_distances_exact(gp, oracle):
     img = rng.integers(1, 4, (8, 9))  # many zero-weight edges
     graph = gp.GridGraph(gp.Image(img), gp.Metric.L1)
     for s in range(0, img.size, 7):
-        d, _ = oracle.propagate(img, [s], metric="l1")
+        d, p0 = oracle.propagate(img, [s], metric="l1")
         r = graph.propagate([s])
         assert np.array_equal(r.dist, d)
-        # parents form a valid shortest-path forest even where heap order is not pinned
+        assert np.array_equal(r.parent, p0)  # heap order on the plateaus
+        # and the parents form a valid shortest-path forest
         for v in range(img.size):
             p = int(r.parent[v])
             if p >= 0:
@@ -73,17 +74,38 @@ def test_l1_distances_exact(gp, oracle):
         _check_tree(np.asarray(r.dist, dtype=np.float32), r.parent, img, 8, "l1", [s])
 
 
-@pytest.mark.parametrize("shape", [(8, 9), (21, 17)])
-def test_l1_plateau_run_completes_with_exact_distances(gp, oracle, shape):
-    """L1 on a plateau image: trees are not pinned to the heap order, but each
-    is a shortest-path tree, so the completed array equals the brute-force
-    distances exactly (integer image)."""
+@pytest.mark.parametrize("shape", [(8, 9), (21, 17), (40, 44)])
+def test_l1_plateau_runs_match_oracle(gp, oracle, shape):
+    """L1 on plateau images (zero-weight edges): the exact heap-order K1 gives
+    the reference's trees, so the whole run -- source sequence, counts and the
+    array -- equals the oracle's (pinned to the reference on L1 by
+    tests/test_oracle.py)."""
     img = np.random.default_rng(12).integers(1, 4, shape) * 5
-    brute = oracle.run(img, "naive", metric="l1")["D"]
-    for kind in (gp.StrategyKind.FILLING_RATE, gp.StrategyKind.NAIVE):
-        run = gp.run_strategy(gp.Image(img), gp.Metric.L1, kind)
+    for kind in ("filling-rate", "naive"):
+        o = oracle.run(img, kind, metric="l1")
+        k = gp.StrategyKind.FILLING_RATE if kind == "filling-rate" else gp.StrategyKind.NAIVE
+        run = gp.run_strategy(gp.Image(img), gp.Metric.L1, k)
         assert run.distances.is_complete
-        assert np.array_equal(run.distances.dist, brute)
+        assert _seq(run) == o["seq"].tolist()
+        assert np.array_equal(run.distances.dist, o["D"])
+        assert run.trace.adjusted_count == o["adjusted"]
+
+
+def test_fp32_zero_pixels_exact_heap(gp, oracle):
+    """fp32 image with adjacent zero pixels (SUM weight 0 between them): the
+    exact heap-order K1 path, against the oracle's propagations and run."""
+    rng = np.random.default_rng(77)
+    img = rng.random((13, 15), dtype=np.float32)
+    img[3:6, 4:9] = 0.0
+    graph = gp.GridGraph(gp.Image(img), gp.Metric.SUM)
+    for s in (0, 50, 64, 194):
+        r = graph.propagate([s])
+        d, p = oracle.propagate(img, [s])
+        assert np.array_equal(r.dist, d) and np.array_equal(r.parent, p)
+    o = oracle.run(img, "filling-rate")
+    run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, gp.StrategyKind.FILLING_RATE)
+    assert _seq(run) == o["seq"].tolist()
+    assert np.array_equal(run.distances.dist, o["D"])
 
 
 @pytest.mark.parametrize("env", [
@@ -236,9 +258,8 @@ def test_global_scratch_propagation_matches_oracle(gp, oracle, shape, conn, metr
         r = graph.propagate([s])
         d, p = oracle.propagate(img, [s], conn=conn, metric=metric)
         assert np.array_equal(np.asarray(r.dist), d), s
-        if metric != "l1":
-            assert np.array_equal(r.parent, p), s
-        else:
+        assert np.array_equal(r.parent, p), s  # L1 plateaus: heap order (exact K1)
+        if metric == "l1":
             _check_tree(np.asarray(r.dist, dtype=np.float32), r.parent, img, conn, metric, [s])
 
 
