@@ -442,9 +442,12 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
         if (!hcnt) hpw = 0;
       }
     }
-    // Debug stamps (GP_DEBUG_SIM).  They also anchor nvcc's schedule of this
-    // phase: without them the four units' load chains were serialised (phase
-    // A 18 us instead of 5 us per commit at 256x256, measured); keep them.
+    // Debug stamps (GP_DEBUG_SIM).  They also anchor ptxas's schedule of this
+    // phase: without them the four units' count loads issue in two pairs
+    // interleaved with the window scans instead of together (SASS, DESIGN.md
+    // section 11) and phase A took 18 us instead of 5 us per commit at
+    // 256x256 (measured); an empty asm memory fence does not reproduce the
+    // effect (GP_PHASEA_ANCHOR=1 compiles to the unanchored binary).  Keep.
     const bool stamp = sim && blockIdx.x == 0 && threadIdx.x == 0 && k0 == wid;
     unsigned q4[4], co4[4], sz4[4];
     uint32_t e4[4];

@@ -1110,11 +1110,6 @@ static const void* prop_kernel(const PropArgs& a, int N, int threads) {
   const bool lean = !a.dbg && !a.D && !a.out_dist && !a.out_dir && a.ts.pre && !a.exact_heap &&
                     !(getenv("GP_PROP_LEAN") && !atoi(getenv("GP_PROP_LEAN")));
   const bool mc = a.g.metric == kSum && a.g.conn == 8 && !(getenv("GP_PROP_MC") && !atoi(getenv("GP_PROP_MC")));
-  // experimental CTA shapes of the lean global-scratch K1 (GP_PROP_THREADS /
-  // GP_PROP_MINB): 768 x 2 and 384 x 4 trees per SM
-  if (!prop_fits_smem(N) && lean && mc && threads == 768 && minb == 2) return (const void*)k_propagate<768, 2, 1, 1>;
-  if (!prop_fits_smem(N) && lean && mc && threads == 384 && minb == 4 && (228 * 1024) / per_cta >= 4)
-    return (const void*)k_propagate<384, 4, 1, 1>;
   if (!prop_fits_smem(N) && threads == 512 && minb == 3 && (228 * 1024) / per_cta >= 3) {
     if (lean) return mc ? (const void*)k_propagate<512, 3, 1, 1> : (const void*)k_propagate<512, 3, 1>;
     return (const void*)k_propagate<512, 3>;
