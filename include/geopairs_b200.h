@@ -87,7 +87,10 @@ int gp_version(void);
 
 /* Image: H x W pixels, row-major.  dtype I64/U8: integer grey levels in
  * [1, 255] (as the reference; rejected otherwise).  dtype F32: finite, >= 0
- * (additive extension).  conn: 8 (reference) or 4 (additive extension). */
+ * (additive extension).  conn: 8 (reference) or 4 (additive extension).
+ * Up to 2^26 pixels; above 65 536 pixels the context serves propagations only
+ * (gp_propagate, gp_propagate_batch, gp_extrema: one whole-GPU relaxation per
+ * tree), as stores and gp_run are limited to 65 536 pixels. */
 int gp_ctx_create(int H, int W, int dtype, const void *pixels, int metric, int conn,
                   gp_ctx **out);
 /* Replace the image of an existing context (same shape/metric/connectivity),

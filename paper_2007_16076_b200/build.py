@@ -11,7 +11,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SOURCES = ["propagate.cu", "propagate_cluster.cu", "commit.cu", "setup.cu", "apgd.cu", "capi.cu"]
+SOURCES = ["propagate.cu", "propagate_cluster.cu", "propagate_big.cu", "commit.cu", "setup.cu", "apgd.cu", "capi.cu"]
 OUT = os.path.join(HERE, "libgeopairs_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -23,6 +23,11 @@ using namespace gp;
 
 static thread_local std::string g_err;
 
+// Pixel limits: the dense N^2 store, gp_run and the batched K1 pack pixel ids
+// in 16 bits; above that a context serves propagations only (whole-GPU K1).
+static constexpr int64_t kMaxPixelsPropagate = (int64_t)1 << 26;
+static constexpr int kMaxPixelsStore = 65536;
+
 static int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
@@ -54,6 +59,8 @@ struct gp_ctx {
   int pos_w = 0;        // every edge weight > 0
   unsigned long long* heap = nullptr;  // exact heap-order K1 scratch (images with zero-weight edges)
   size_t heap_trees = 0;
+  unsigned char* big = nullptr;  // scratch of the whole-GPU K1 (contexts above 65 536 pixels)
+  unsigned* h_flag = nullptr;    // pinned pass flag of the whole-GPU K1
   uint32_t* list[2] = {nullptr, nullptr};  // unfilled-pair lists (late phase)
   int* h_cnt2 = nullptr;     // pinned: two count snapshots (host-row rounds)
   Ctl* h_ctl2 = nullptr;     // pinned: two control-block snapshots
@@ -159,7 +166,10 @@ extern "C" int gp_ctx_create(int H, int W, int dtype, const void* pixels, int me
                              gp_ctx** out) {
   if (!out || !pixels) return fail(GP_EINVAL, "null argument");
   if (H < 1 || W < 1 || (int64_t)H * W < 2) return fail(GP_EINVAL, "image must contain at least 2 pixels");
-  if ((int64_t)H * W > 65536) return fail(GP_EINVAL, "images above 65536 pixels are not supported (dense N^2 store)");
+  // above 65 536 pixels a context serves propagations only (the dense N^2
+  // store and gp_run need 16-bit pixel ids); the limit here keeps ids in 32 bits
+  if ((int64_t)H * W > kMaxPixelsPropagate)
+    return fail(GP_EINVAL, "images above 2^26 pixels are not supported");
   if (conn != 4 && conn != 8) return fail(GP_EINVAL, "connectivity must be 4 or 8");
   if (metric < 0 || metric > 2) return fail(GP_EINVAL, "unknown metric");
   const int N = H * W;
@@ -216,6 +226,8 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
   cudaFree(c->bar);
   cudaFree(c->scratch);
   cudaFree(c->heap);
+  cudaFree(c->big);
+  if (c->h_flag) cudaFreeHost(c->h_flag);
   if (c->st) cudaStreamDestroy(c->st);
   if (c->st2) cudaStreamDestroy(c->st2);
   if (c->st3) cudaStreamDestroy(c->st3);
@@ -300,6 +312,19 @@ static float default_delta(const gp_ctx* c) {
   return (float)(factor * c->mean_w);
 }
 
+static bool is_big(const gp_ctx* c) { return c->g.N > kMaxPixelsStore; }
+
+// One propagation of a context above 65 536 pixels (propagate_big.cu) into
+// device buffers dist (fp32 bits) and code (parent window codes).
+static int big_prop(gp_ctx* c, const int* d_src, int ns, uint32_t* d_dist, uint8_t* d_code, cudaStream_t st) {
+  const int exact = c->pos_w ? 0 : 1;
+  const size_t need = big_scratch_bytes(c->g.N, 1);
+  if (!c->big) CUDA_TRY(dalloc(&c->big, need));
+  if (!c->h_flag) CUDA_TRY(cudaHostAlloc(&c->h_flag, 4, cudaHostAllocDefault));
+  CUDA_TRY(launch_propagate_big(c->g, c->d_img, d_src, ns, exact, d_dist, d_code, c->big, c->h_flag, st));
+  return GP_OK;
+}
+
 extern "C" int gp_propagate(gp_ctx* c, const int32_t* sources, int nsrc, float* dist_out,
                             int32_t* parent_out) {
   if (!c || !sources || nsrc < 1) return fail(GP_EINVAL, "at least one source pixel is required");
@@ -309,8 +334,6 @@ extern "C" int gp_propagate(gp_ctx* c, const int32_t* sources, int nsrc, float* 
     if (sources[i] < 0 || sources[i] >= N) return fail(GP_EINVAL, "source out of range");
     if (seen[sources[i]]++) return fail(GP_EINVAL, "duplicate source pixels");
   }
-  int rc = ensure_scratch(c, 1);
-  if (rc) return rc;
   DevBuf<int> d_src;
   DevBuf<float> d_dist;
   DevBuf<uint8_t> d_dir;
@@ -318,13 +341,19 @@ extern "C" int gp_propagate(gp_ctx* c, const int32_t* sources, int nsrc, float* 
   CUDA_TRY(d_dist.alloc(N));
   CUDA_TRY(d_dir.alloc(N));
   CUDA_TRY(cudaMemcpyAsync(d_src.p, sources, nsrc * 4, cudaMemcpyHostToDevice, c->st));
-  PropArgs a = base_prop(c);
-  a.src = d_src.p;
-  a.ns = nsrc;
-  a.out_dist = d_dist.p;
-  a.out_dir = d_dir.p;
-  a.delta = default_delta(c);
-  CUDA_TRY(launch_propagate(a, 1, c->st));
+  if (is_big(c)) {
+    if (int rc = big_prop(c, d_src.p, nsrc, reinterpret_cast<uint32_t*>(d_dist.p), d_dir.p, c->st)) return rc;
+  } else {
+    int rc = ensure_scratch(c, 1);
+    if (rc) return rc;
+    PropArgs a = base_prop(c);
+    a.src = d_src.p;
+    a.ns = nsrc;
+    a.out_dist = d_dist.p;
+    a.out_dir = d_dir.p;
+    a.delta = default_delta(c);
+    CUDA_TRY(launch_propagate(a, 1, c->st));
+  }
   std::vector<uint8_t> dir(N);
   if (dist_out) CUDA_TRY(cudaMemcpyAsync(dist_out, d_dist.p, N * 4, cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(cudaMemcpyAsync(dir.data(), d_dir.p, N, cudaMemcpyDeviceToHost, c->st));
@@ -342,6 +371,13 @@ extern "C" int gp_propagate(gp_ctx* c, const int32_t* sources, int nsrc, float* 
 extern "C" int gp_propagate_batch(gp_ctx* c, const int32_t* src_dev, int k, float* tdist_dev,
                                   uint8_t* dir_dev, void* stream) {
   if (!c || !src_dev || k < 0) return fail(GP_EINVAL, "bad arguments");
+  if (is_big(c)) {  // one whole-GPU propagation per source
+    for (int i = 0; i < k; i++)
+      if (int r = big_prop(c, src_dev + i, 1, reinterpret_cast<uint32_t*>(tdist_dev + (size_t)i * c->g.N),
+                           dir_dev + (size_t)i * c->g.N, (cudaStream_t)stream))
+        return r;
+    return GP_OK;
+  }
   int rc = ensure_scratch(c, (size_t)k);
   if (rc) return rc;
   PropArgs a = base_prop(c);
@@ -409,12 +445,24 @@ static int extrema_device(gp_ctx* c, int* centroid, float* dfc_dev, std::vector<
   int* d_src = nullptr;
   int* d_cen = nullptr;
   float* d_fb = nullptr;
-  int rc = ensure_scratch(c, 1);
-  if (rc) return rc;
   CUDA_TRY(ws_get(c, WS_BORDER, &d_src, border.size() + 1));
   CUDA_TRY(ws_get(c, WS_CEN, &d_cen, 1));
   CUDA_TRY(ws_get(c, WS_FB, &d_fb, N));
   CUDA_TRY(cudaMemcpyAsync(d_src, border.data(), border.size() * 4, cudaMemcpyHostToDevice, c->st));
+  if (is_big(c)) {  // whole-GPU propagations (contexts above 65 536 pixels)
+    uint8_t* d_code = nullptr;
+    CUDA_TRY(ws_get(c, WS_CS_DIR, &d_code, N));
+    if (int r = big_prop(c, d_src, (int)border.size(), reinterpret_cast<uint32_t*>(d_fb), d_code, c->st)) return r;
+    CUDA_TRY(launch_argmax_first(d_fb, N, d_cen, c->st));
+    if (int r = big_prop(c, d_cen, 1, reinterpret_cast<uint32_t*>(dfc_dev), d_code, c->st)) return r;
+    dfc_host.resize(N);
+    CUDA_TRY(cudaMemcpyAsync(centroid, d_cen, 4, cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaMemcpyAsync(dfc_host.data(), dfc_dev, (size_t)N * 4, cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaStreamSynchronize(c->st));
+    return GP_OK;
+  }
+  int rc = ensure_scratch(c, 1);
+  if (rc) return rc;
   PropArgs a = base_prop(c);
   a.src = d_src;
   a.ns = (int)border.size();
@@ -463,7 +511,7 @@ extern "C" int gp_extrema(gp_ctx* c, int32_t* centroid, float* dfc_out, int32_t*
 extern "C" int gp_store_create(int64_t n, gp_store** out) {
   if (!out) return fail(GP_EINVAL, "null argument");
   if (n < 2) return fail(GP_EINVAL, "need at least 2 pixels");
-  if (n > 65536) return fail(GP_ENOMEM, "stores above 65536 pixels are not supported");
+  if (n > kMaxPixelsStore) return fail(GP_ENOMEM, "stores above 65536 pixels are not supported");
   gp_store* s = new gp_store();
   s->n = n;
   s->L = make_layout((int)n, 1, (int)n);  // no image yet: raster columns

@@ -618,7 +618,6 @@ __device__ __forceinline__ unsigned fill_root_row(const CommitArgs& a, int slot,
   const float* tdp = a.ts.tdp + off;
   uint32_t* row = a.mark + (size_t)s * L.RW;
   const uint32_t scol = mcol(L, (uint32_t)s);
-  const uint32_t sbit = 1u << (scol & 31);
   unsigned mine = 0;
   const int stride = gridDim.x * blockDim.x;
   for (int x0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); x0 < N; x0 += stride) {

@@ -67,6 +67,11 @@ size_t prop_scratch_bytes(int N);
 bool prop_fits_smem(int N);
 int prop_trees_per_sm(int N);
 cudaError_t launch_propagate(PropArgs a, int ntrees, cudaStream_t st);
+// propagation-only contexts above 65 536 pixels (propagate_big.cu): one tree on the whole GPU
+size_t big_scratch_bytes(int N, int exact);
+cudaError_t launch_propagate_big(const Grid& g, const float* img, const int* src, int ns, int exact,
+                                 uint32_t* dist_out, uint8_t* code_out, unsigned char* scratch,
+                                 unsigned* hflag, cudaStream_t st);
 // cluster variant (propagate_cluster.cu): one tree per 2-CTA cluster, state in DSMEM
 size_t prop_cluster_smem(int N);
 size_t prop_cluster_scratch(int N);

@@ -326,3 +326,31 @@ def test_cluster_and_single_cta_k1_runs_identical(gp, monkeypatch, shape, conn, 
         out.append(([s for _, s, _ in run.trace.samples], [f for _, _, f in run.trace.samples], h))
         del run, Dd
     assert out[0] == out[1]
+
+
+@pytest.mark.parametrize("shape,metric,conn", [((300, 300), "sum", 8), ((257, 263), "mean", 4),
+                                               ((260, 260), "l1", 8)])
+def test_propagation_contexts_above_65536_pixels(gp, oracle, shape, metric, conn):
+    """Images above 65 536 pixels serve propagations (the reference's
+    GridGraph has no size limit): the whole-GPU K1 against the oracle --
+    distances and parents, L1 plateaus through the sequential heap path --
+    and the extrema context; stores and runs of that size are refused."""
+    rng = np.random.default_rng(sum(shape))
+    img = rng.integers(1, 256, shape)
+    if metric == "l1":
+        img = (img // 64 + 1) * 10  # plateaus
+    m = {"sum": gp.Metric.SUM, "mean": gp.Metric.MEAN, "l1": gp.Metric.L1}[metric]
+    graph = gp.GridGraph(gp.Image(img), m, connectivity=conn)
+    N = img.size
+    for srcs in ([0], [N - 1], [N // 2 + 7], [5, N // 3, N - 40]):
+        r = graph.propagate(srcs)
+        d, p = oracle.propagate(img, srcs, conn=conn, metric=metric)
+        assert np.array_equal(r.dist, d), srcs
+        assert np.array_equal(r.parent, p), srcs
+    if metric != "l1":
+        ctx = gp.compute_extrema_context(gp.Image(img), m, connectivity=conn)
+        cen, dfc, ext = oracle.extrema(img, conn=conn, metric=metric)
+        assert ctx.centroid == cen
+        assert np.array_equal(np.asarray(ctx.dist_from_c), dfc) and np.array_equal(np.asarray(ctx.ext), ext)
+    with pytest.raises(MemoryError):
+        gp.DistanceArray(N, force=True)
