@@ -151,44 +151,42 @@ def _config_dict(spec, P: int, P_adj: int, world: int) -> dict:
 
 def _port_sample(img, spec, P: int, C: int, target_s: float, nthreads: int, m2: int = 0):
     """The oracle port's real loop (selection + propagation + tree fill) over
-    two prefixes of the run (M1 < M2 commits, timed inside the loop,
-    allocation excluded).  The whole image is extrapolated from the marginal
-    segment M1..M2 (first-touch effects of the first commits excluded) in
-    proportion to ancestor visits: t_image = (t2 - t1) * C / (C2 - C1), C =
-    the run's visits (sum of tree depths).  The fill walks every ancestor pair
-    of each tree (reference _kernels.py:96-115) and visits per commit decline
-    over the run, so this undercounts the per-commit propagation cost of late
-    commits: a conservative (low) CPU time."""
+    the first M2 commits of the run, timed inside the loop with a timestamp
+    per commit (allocation excluded).  The whole image is extrapolated from
+    the marginal segment M1..M2 (M1 = 32: first-touch effects of the first
+    commits excluded) in proportion to ancestor visits: t_image = (t2 - t1) *
+    C / (C2 - C1), C = the run's visits (sum of tree depths).  The fill walks
+    every ancestor pair of each tree (reference _kernels.py:96-115) and visits
+    per commit decline over the run, so this undercounts the per-commit
+    propagation cost of late commits: a conservative (low) CPU time."""
     from oracle import oracle as O
 
     m1 = min(spec.n, 32)
-    t0 = 0.0
     if not m2:  # calibration: marginal per-commit time beyond the first touches
-        m0 = min(spec.n, 8)
-        t0 = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m0)["loop_seconds"]
-    r1 = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m1)
-    if not m2:
-        per = (r1["loop_seconds"] - t0) / max(m1 - m0, 1)
-        m2 = int(min(spec.n, m1 + max(m1, 0.6 * target_s / max(per, 1e-6))))
-    r2 = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m2)
-    t1, t2 = r1["loop_seconds"], r2["loop_seconds"]
-    c1, c2 = int(r1["visits"].sum()), int(r2["visits"].sum())
-    k1, k2 = int(r1["raw"]), int(r2["raw"])
+        r = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m1)
+        cs = r["commit_seconds"]
+        per = (cs[-1] - cs[7]) / max(len(cs) - 8, 1)
+        m2 = int(min(spec.n, m1 + max(m1, 0.8 * target_s / max(per, 1e-6))))
+    r = O.run(img, spec.strategy, conn=spec.conn, nthreads=nthreads, max_steps=m2)
+    cs, vis = r["commit_seconds"], np.cumsum(r["visits"])
+    k2 = int(r["raw"])
+    t1, t2 = float(cs[m1 - 1]), float(cs[k2 - 1])
+    c1, c2 = int(vis[m1 - 1]), int(vis[k2 - 1])
     per_visit = (t2 - t1) / max(c2 - c1, 1)
     ms_image = per_visit * C * 1e3
     return {
         "value": spec.total_pairs / (ms_image / 1e3), "unit": "pairs/s", "cores": nthreads,
         "cores_available": os.cpu_count(), "kind": "port",
         "ms_per_image": ms_image,
-        "ms_per_image_kind": (f"extrapolated: marginal time of commits {k1}..{k2} per ancestor visit x the run's "
+        "ms_per_image_kind": (f"extrapolated: marginal time of commits {m1}..{k2} per ancestor visit x the run's "
                               f"C={C} visits (P={P} commits)"),
-        "per_commit_ms": (t2 - t1) / max(k2 - k1, 1) * 1e3, "commits_timed": k2,
-        "seconds": t0 + t1 + t2, "m2": k2,
-        "prefix_pairs_per_s": r2["filled"] / t2,
+        "per_commit_ms": (t2 - t1) / max(k2 - m1, 1) * 1e3, "commits_timed": k2,
+        "seconds": t2, "m2": k2,
+        "prefix_pairs_per_s": r["filled"] / r["loop_seconds"],
         "sample": (f"oracle/oracle.c (C restatement of the reference loop; the reference rejects fp32 images) "
-                   f"on {nthreads} of {os.cpu_count()} host threads: the first {k1} and {k2} commits of the "
-                   f"{spec.name} filling-rate run in {t1:.2f}s / {t2:.2f}s; commits {k1}..{k2} took "
-                   f"{(t2 - t1) / max(k2 - k1, 1) * 1e3:.1f} ms each ({(c2 - c1) / max(k2 - k1, 1) / 1e6:.1f} M "
+                   f"on {nthreads} of {os.cpu_count()} host threads: the first {k2} commits of the "
+                   f"{spec.name} filling-rate run in {t2:.2f}s; commits {m1}..{k2} took "
+                   f"{(t2 - t1) / max(k2 - m1, 1) * 1e3:.1f} ms each ({(c2 - c1) / max(k2 - m1, 1) / 1e6:.1f} M "
                    f"visits each); whole image extrapolated by visits to {ms_image / 1e3:.0f}s"),
     }
 
@@ -236,7 +234,7 @@ def run_reference(args, spec, img, world, rank):
     nthreads = os.cpu_count() or 1
     P, P_adj, C = _golden_counts(args.config)
     vals, samples = [], []
-    budget = max(3.0, min(args.cpu_seconds, 180.0 / (args.warmup + args.steps)))  # seconds per step
+    budget = max(2.0, min(args.cpu_seconds, 100.0 / (args.warmup + args.steps)))  # sampled seconds per step
     m2 = 0
     for i in range(args.warmup + args.steps):
         r = _port_sample(img, spec, P, C, budget, nthreads, m2)

@@ -356,7 +356,7 @@ int or_extrema(int H, int W, int conn, int metric, int isf, const void *px,
 int or_run(int H, int W, int conn, int metric, int isf, const void *px, int kind,
            int naive_with_tree, int nthreads, void *D_out, int32_t *seq_out,
            int64_t *new_out, int64_t *visits_out, int64_t *walked_out, int64_t *stats,
-           int64_t max_steps, double *loop_seconds) {
+           int64_t max_steps, double *loop_seconds, double *commit_seconds) {
     int64_t n = (int64_t)H * W;
     img_t im = {H, W, conn, metric, isf, isf ? NULL : (const int64_t *)px,
                 isf ? (const float *)px : NULL};
@@ -366,6 +366,7 @@ int or_run(int H, int W, int conn, int metric, int isf, const void *px, int kind
     int32_t *par = malloc(n * sizeof(int32_t));
     int32_t *rank = malloc(n * sizeof(int32_t));
     if (!st.mark || !st.cnt || !heap || !td || !par || !rank) return -1;
+#pragma omp parallel for num_threads(nthreads > 0 ? nthreads : 1) schedule(static)
     for (int64_t i = 0; i < n; i++) {
         st.mark[i * n + i] = 1;
         if (isf) { float *D = D_out; for (int64_t j = 0; j < n; j++) D[i * n + j] = (i == j) ? 0.0f : -1.0f; }
@@ -413,6 +414,11 @@ int or_run(int H, int W, int conn, int metric, int isf, const void *px, int kind
         new_out[count] = newp;
         if (visits_out) visits_out[count] = visits;
         if (walked_out) walked_out[count] = walked;
+        if (commit_seconds) { /* cumulative loop time after each commit (CPU-baseline sampling) */
+            struct timespec tc;
+            clock_gettime(CLOCK_MONOTONIC, &tc);
+            commit_seconds[count] = (tc.tv_sec - t0.tv_sec) + 1e-9 * (tc.tv_nsec - t0.tv_nsec);
+        }
         count++;
     }
     clock_gettime(CLOCK_MONOTONIC, &t1);

@@ -46,7 +46,7 @@ def lib():
         i32, i64 = ctypes.c_int, ctypes.c_int64
         L.or_propagate.argtypes = [i32, i32, i32, i32, i32, P, P, i32, P, P]
         L.or_extrema.argtypes = [i32, i32, i32, i32, i32, P, P, P, P]
-        L.or_run.argtypes = [i32, i32, i32, i32, i32, P, i32, i32, i32, P, P, P, P, P, P, i64, P]
+        L.or_run.argtypes = [i32, i32, i32, i32, i32, P, i32, i32, i32, P, P, P, P, P, P, i64, P, P]
         L.or_replay_prefix.argtypes = [i32, i32, i32, i32, i32, P, P, i64, i32, i32, P]
         L.or_fill_tree.argtypes = [i64, i32, P, P, P, P, P, P]
         L.or_fill_tree.restype = i64
@@ -114,16 +114,18 @@ def run(pixels, kind="filling-rate", *, conn: int = 8, metric="sum", naive_with_
     walked = np.zeros(n, dtype=np.int64)
     stats = np.zeros(8, dtype=np.int64)
     loop_s = np.zeros(1, dtype=np.float64)
+    commit_s = np.zeros(n, dtype=np.float64)
     rc = lib().or_run(H, W, conn, _metric(metric), isf, _ptr(px), KINDS[getattr(kind, "value", kind)],
                       int(naive_with_tree), nthreads, _ptr(D), _ptr(seq), _ptr(new), _ptr(visits),
-                      _ptr(walked), _ptr(stats), n if max_steps is None else max_steps, _ptr(loop_s))
+                      _ptr(walked), _ptr(stats), n if max_steps is None else max_steps, _ptr(loop_s),
+                      _ptr(commit_s))
     if rc not in (0,) and not (max_steps is not None and rc == 0):
         raise RuntimeError(f"oracle run failed rc={rc}")
     P = int(stats[0])
     return {
         "D": D, "seq": seq[:P].astype(np.int64), "new": new[:P], "visits": visits[:P], "walked": walked[:P],
         "raw": P, "adjusted": int(stats[1]), "centroid": int(stats[3]), "filled": int(stats[4]),
-        "loop_seconds": float(loop_s[0]),
+        "loop_seconds": float(loop_s[0]), "commit_seconds": commit_s[:P],
     }
 
 
