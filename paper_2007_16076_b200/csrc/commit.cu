@@ -1180,17 +1180,24 @@ __device__ unsigned radix_kth(const unsigned* keys, int N, unsigned K, unsigned 
     __syncthreads();
     const unsigned prefix = s_prefix, mask = s_mask;
     if (!s_all) {
-      for (int v0 = tid; v0 < N; v0 += TK_UB * blockDim.x) {
+      // warp-uniform trips (match_any below needs every lane)
+      for (int vb = tid & ~31; vb < N; vb += TK_UB * blockDim.x) {
+        const int v0 = vb + (tid & 31);
         unsigned kk[TK_UB];
 #pragma unroll
         for (int j = 0; j < TK_UB; j++) {
           const int v = v0 + j * blockDim.x;
           kk[j] = v < N ? __ldcg(&keys[v]) : 0xFFFFFFFFu;
         }
+        // warp-aggregated: keys cluster (few distinct counts), so per-key
+        // shared atomics on one bin serialised the pass
 #pragma unroll
-        for (int j = 0; j < TK_UB; j++)
-          if (kk[j] != 0xFFFFFFFFu && kk[j] <= lim && (kk[j] & mask) == prefix)
-            atomicAdd(&hist[(kk[j] >> shift) & 255u], 1u);
+        for (int j = 0; j < TK_UB; j++) {
+          const bool in = kk[j] != 0xFFFFFFFFu && kk[j] <= lim && (kk[j] & mask) == prefix;
+          const unsigned bin = in ? (kk[j] >> shift) & 255u : 256u;
+          const unsigned peers = __match_any_sync(0xffffffffu, bin);
+          if (in && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&hist[bin], (unsigned)__popc(peers));
+        }
       }
     }
     __syncthreads();
@@ -1314,16 +1321,23 @@ __global__ void __launch_bounds__(1024) k_topk(CommitArgs a, int K, int Q, int* 
     }
     __syncthreads();
   }
-  if (tid == 0) {
+  // slots from the bump allocator and the claims, all threads (a serial loop
+  // of K global read-modify-writes by one thread was ~half of this kernel)
+  {
     const int n = min(s_n, K);
     Ctl* c = a.ctl;
-    for (int i = 0; i < n; i++) {
-      slots[i] = c->nslots++;
+    const int base = *(volatile int*)&c->nslots;
+    for (int i = tid; i < n; i += blockDim.x) {
+      slots[i] = base + i;
       a.claimed[cands[i]] = 1;
     }
-    c->ncand = n;
-    c->total_props += n;
-    c->batches++;
+    __syncthreads();  // every thread has read nslots
+    if (tid == 0) {
+      c->nslots = base + n;
+      c->ncand = n;
+      c->total_props += n;
+      c->batches++;
+    }
   }
 }
 

@@ -54,6 +54,9 @@ extern __shared__ __align__(16) unsigned char g_smem[];
 #ifndef GP_UE
 #define GP_UE 4
 #endif
+#ifndef GP_E5
+#define GP_E5 1  // parents per thread and iteration in the sibling-offset pass (E5; 256^2: 1 -> 578.6, 2 -> 586.7, 4 -> 599.5 ms)
+#endif
 
 constexpr int HIST_SMEM = 4096;  // depth-histogram bins in the shared-memory variant
 constexpr int HIST_G = 1024;     // depth-histogram bins in smem (global-scratch variant)
@@ -833,13 +836,15 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
   // One thread per parent p walks its <= 8 neighbours in increasing id
   // (= neighbour order) and assigns each child its sibling offset; every
   // non-root pixel is written by its parent's thread, the root by itself.
-  // Two parents per iteration: their children's sizes are loaded together.
-  for (int p0 = tid; p0 < N; p0 += 2 * nthr) {
-    unsigned mask[2] = {0u, 0u};
-    unsigned szc[2][9];
+  // GP_E5 parents per iteration (their children's sizes loaded together; one
+  // measured best: the single-parent loop keeps more warps issuing).
+  for (int p0 = tid; p0 < N; p0 += GP_E5 * nthr) {
+    unsigned mask[GP_E5];
+    unsigned szc[GP_E5][9];
 #pragma unroll
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < GP_E5; b++) {
       const int pp = p0 + b * nthr;
+      mask[b] = 0u;
       if (pp >= N) continue;
       if (code_get(vcode, pp) == GP_ROOT) pj[pp] = (uint32_t)pp;
       int pr, pc;
@@ -854,14 +859,14 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       }
     }
 #pragma unroll
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < GP_E5; b++) {
       const int pp = p0 + b * nthr;
 #pragma unroll
       for (int k = 0; k < 9; k++)
         szc[b][k] = ((mask[b] >> k) & 1u) ? rd16(&szB[pp + (k / 3 - 1) * g.W + (k % 3 - 1)]) : 0u;
     }
 #pragma unroll
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < GP_E5; b++) {
       const int pp = p0 + b * nthr;
       unsigned offs = 0;
 #pragma unroll
