@@ -1188,7 +1188,8 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       ca.plist[1] = c->list[1];
       // rounds per host check; with host rows, single rounds once few rows
       // are open, so the rows still to copy after the last commit are few
-      const int chunk = 6;
+      int chunk = 6;
+      if (const char* e = getenv("GP_ROUNDS_PER_SYNC")) chunk = std::max(1, atoi(e));
       auto prop_batch = [&](int gated) -> int {
         EvPair f;
         CUDA_TRY(evp.pair(f));

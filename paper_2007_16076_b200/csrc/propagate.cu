@@ -54,6 +54,9 @@ extern __shared__ __align__(16) unsigned char g_smem[];
 #ifndef GP_UE
 #define GP_UE 4
 #endif
+#ifndef GP_RR
+#define GP_RR 2  // relaxation rounds of (item, edge) pairs in flight per thread (global variant)
+#endif
 #ifndef GP_E5
 #define GP_E5 1  // parents per thread and iteration in the sibling-offset pass (E5; 256^2: 1 -> 578.6, 2 -> 586.7, 4 -> 599.5 ms)
 #endif
@@ -450,7 +453,7 @@ __global__ void __launch_bounds__(THR, MINB) k_propagate(PropArgs a) {
       // worklist is read from shared memory directly while it fits there; the
       // window offsets come from packed constants, one unsigned compare per
       // bound; the appends of the RR rounds share one counter update.
-      constexpr int RR = 2;  // measured: 1 -> 615, 2 -> 600, 3 -> 609, 4 -> 614, 6 -> 659 ms per 256^2 image
+      constexpr int RR = GP_RR;  // measured: 1 -> 615, 2 -> 600, 3 -> 609, 4 -> 614, 6 -> 659 ms per 256^2 image
       const int items = n * 8;
       const bool wl_fits = n <= wl.cap;
       const uint16_t* lsm = wl.s[cur];
