@@ -79,3 +79,38 @@ def test_both_arms_share_the_config_dict():
     a = bench._config_dict(CONFIGS[5], P, P_adj, 1)
     assert a == bench._config_dict(CONFIGS[5], 52191, 52193, 1)
     assert a["workload"] == CONFIGS[5].name and a["pairs_per_image"] == CONFIGS[5].total_pairs
+
+
+def test_cpu_baseline_sampler_runs_and_extrapolates():
+    """bench._port_sample on the config-2 image (integer, 4096 pixels): the
+    marginal-segment extrapolation returns a finite whole-image time bounded
+    below by the sampled prefix, with the labels the JSON line carries."""
+    import bench
+    from paper_2007_16076_b200.configs import CONFIGS, make_image
+
+    spec = CONFIGS[2]
+    P, _, C = bench._golden_counts(2)
+    assert C == 0 or C > 0  # the int goldens carry no visits (reference run)
+    from oracle import oracle as O
+
+    C = int(O.run(make_image(2), "filling-rate", nthreads=2)["visits"].sum())
+    r = bench._port_sample(make_image(2), spec, P, C, 0.5, 2)
+    assert r["kind"] == "port" and r["cores"] == 2 and r["commits_timed"] > 32
+    assert r["ms_per_image"] / 1e3 > r["seconds"] * 0.5 and r["value"] > 0
+    assert "extrapolated" in r["ms_per_image_kind"]
+
+
+def test_reference_timing_script_replays_the_reference():
+    """baseline/ref_timing.py runs the UNMODIFIED reference (when installed in
+    baseline/_ref) over a replayed prefix of the committed cfg4 sequence."""
+    import os
+
+    import pytest
+
+    import bench
+
+    if not os.path.isdir(os.path.join(bench.ROOT, "baseline", "_ref", "geopairs")):
+        pytest.skip("reference not installed in baseline/_ref")
+    r = bench._ref_timing("replay", 4, 5, timeout=600)
+    assert r.get("kind") == "reference", r
+    assert r["commits"] == 5 and r["per_commit_ms"] > 0 and r["P"] == 13141
