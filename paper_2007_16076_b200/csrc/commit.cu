@@ -334,10 +334,12 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
 #define GP_FQ_CAP 4096
 #endif
 constexpr int FQ_CAP = GP_FQ_CAP;
-// phase-A schedule anchors (see the comment in fill_tree_cta): 0 = the debug
-// stamps (default), 1 = empty asm memory fences, 2 = none (measured slower)
+// Phase-A schedule anchors (see fill_tree_cta): 1 = __syncwarp() between the
+// four units' load stages (default), 0 = the round-1 debug stamps, 2 = none.
+// 256^2 commit loop: 898 / 908 / 1171 ms (an empty asm memory fence compiles
+// to the same binary as none).
 #ifndef GP_PHASEA_ANCHOR
-#define GP_PHASEA_ANCHOR 0
+#define GP_PHASEA_ANCHOR 1
 #endif
 struct FillQ {
   uint2 desc[FQ_CAP];
@@ -442,13 +444,15 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
         if (!hcnt) hpw = 0;
       }
     }
-    // Debug stamps (GP_DEBUG_SIM).  They also anchor ptxas's schedule of this
-    // phase: without them the four units' count loads issue in two pairs
-    // interleaved with the window scans instead of together (SASS, DESIGN.md
-    // section 11) and phase A took 18 us instead of 5 us per commit at
-    // 256x256 (measured); an empty asm memory fence does not reproduce the
-    // effect (GP_PHASEA_ANCHOR=1 compiles to the unanchored binary).  Keep.
+    // Schedule anchors.  Left to itself ptxas issues the four units' count
+    // loads in two pairs interleaved with the window scans instead of
+    // together (SASS), and phase A takes 18 us instead
+    // of 5 us per commit at 256x256.  A __syncwarp() after each load stage
+    // (memory ordering among the warp's lanes) keeps the stages apart; the
+    // round-1 build got the same effect from dead debug stamps.
+#if GP_PHASEA_ANCHOR == 0
     const bool stamp = sim && blockIdx.x == 0 && threadIdx.x == 0 && k0 == wid;
+#endif
     unsigned q4[4], co4[4], sz4[4];
     uint32_t e4[4];
 #pragma unroll
@@ -482,10 +486,10 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
         if (cn4[i]) lnew += fill_unit<(G > 4 ? 4 : G)>(a, slot, s, (int)blockIdx.x + (k0 + i * nw) * NB);
       continue;
     }
-#if GP_PHASEA_ANCHOR == 0
+#if GP_PHASEA_ANCHOR == 1
+    __syncwarp();
+#elif GP_PHASEA_ANCHOR == 0
     if (stamp) sim[4] = gtimer() - t_a0 + (unsigned long long)(q4[0] + q4[1] + q4[2] + q4[3]) * 0ull;
-#elif GP_PHASEA_ANCHOR == 1
-    asm volatile("" ::"r"(q4[0]), "r"(q4[1]), "r"(q4[2]), "r"(q4[3]) : "memory");
 #endif
     unsigned my4[4], c04[4], tk4[4];
     int cv4[4];
@@ -495,10 +499,10 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
       const int u_l = (int)(e4[i] & 0xFFFFu);
       cv4[i] = (my4[i] && u_l != s) ? __ldcg(&a.cnt[u_l]) : 0;
     }
-#if GP_PHASEA_ANCHOR == 0
+#if GP_PHASEA_ANCHOR == 1
+    __syncwarp();
+#elif GP_PHASEA_ANCHOR == 0
     if (stamp) sim[5] = gtimer() - t_a0 + (unsigned long long)(tk4[0] + tk4[3]) * 0ull;
-#elif GP_PHASEA_ANCHOR == 1
-    asm volatile("" ::"r"(tk4[0]), "r"(tk4[3]) : "memory");
 #endif
     // first windows of the four units: one reservation, independent chains
     unsigned nop4[4], inc4[4], wt4[4], wsum = 0;
@@ -515,10 +519,10 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
       fq_write(Q, lane, (unsigned)base, wt4[i], inc4[i], nop4[i], (int)q4[i], e4[i], sz4[i], c04[i]);
       base += (int)wt4[i];
     }
-#if GP_PHASEA_ANCHOR == 0
+#if GP_PHASEA_ANCHOR == 1
+    __syncwarp();
+#elif GP_PHASEA_ANCHOR == 0
     if (stamp) sim[6] = gtimer() - t_a0;
-#elif GP_PHASEA_ANCHOR == 1
-    asm volatile("" ::: "memory");
 #endif
 #pragma unroll
     for (int i = 0; i < 4; i++) {
