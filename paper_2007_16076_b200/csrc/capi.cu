@@ -241,7 +241,7 @@ extern "C" int gp_ctx_num_pixels(const gp_ctx* c) { return c ? c->g.N : 0; }
 
 enum { WS_SEQ, WS_NEW, WS_SRC, WS_SLOT_OF, WS_RANK, WS_EXT, WS_SELKEY, WS_FLAGS, WS_CTL, WS_DFC,
        WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK, WS_EXTK, WS_EXTT, WS_CSET,
-       WS_VERIFY, WS_CS_SRC, WS_CS_DIST, WS_CS_DIR, WS_CS_PAR };
+       WS_VERIFY, WS_CS_SRC, WS_CS_DIST, WS_CS_DIR, WS_CS_PAR, WS_LB, WS_LBHITS, WS_LBTINB };
 
 template <typename T>
 static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
@@ -1186,6 +1186,25 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       }
       ca.plist[0] = c->list[0];
       ca.plist[1] = c->list[1];
+      // list mode: several commits per grid step (k_commit_lb); GP_LIST_BATCH=0: one per step
+      if (ca.cand && ca.strategy != kNaive && commit_split() &&
+          !(getenv("GP_LIST_BATCH") && !atoi(getenv("GP_LIST_BATCH")))) {
+        LbCtl* d_lb = nullptr;
+        unsigned long long* d_hits = nullptr;
+        CUDA_TRY(ws_get(c, WS_LB, &d_lb, 1));
+        CUDA_TRY(ws_get(c, WS_LBHITS, &d_hits, (size_t)c->list_cap));
+        CUDA_TRY(cudaMemsetAsync(d_lb, 0, sizeof(LbCtl), st));
+        ca.lb = d_lb;
+        ca.lb_hits = d_hits;
+        ca.lb_debug = getenv("GP_LB_DEBUG") && atoi(getenv("GP_LB_DEBUG"));
+        ca.lb_pack_min = 65536;
+        if (const char* e = getenv("GP_LB_PACK_MIN")) ca.lb_pack_min = (unsigned)std::max(0, atoi(e));
+        if (!(getenv("GP_LB_PACK") && !atoi(getenv("GP_LB_PACK")))) {
+          uint32_t* d_tinb = nullptr;
+          CUDA_TRY(ws_get(c, WS_LBTINB, &d_tinb, (size_t)N * 16));
+          ca.lb_tinb = d_tinb;
+        }
+      }
       // rounds per host check; with host rows, single rounds once few rows
       // are open, so the rows still to copy after the last commit are few
       int chunk = 6;
@@ -1407,6 +1426,16 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
               h[1] / nt / 1e3, h[2] / nt / 1e3, h[3] / nt / 1e3, h[4] / nt / 1e3, h[5] / nt / 1e3,
               h[6] / nt / 1e3, h[7] / nt / 1e3, h[8] / nt / 1e3, h[10] / nt, h[11] / nt, h[12] / nt,
               h[13], h[14]);
+    }
+    if (ca.lb && ca.lb_debug) {
+      LbCtl h;
+      CUDA_TRY(cudaMemcpy(&h, ca.lb, sizeof(h), cudaMemcpyDeviceToHost));
+      const double nb = h.dbg[0] ? (double)h.dbg[0] : 1.0;
+      fprintf(stderr, "[gp list batch] batches %llu commits %llu (%.2f per batch, offered %.2f) collects %llu | per batch (us): "
+              "select %.2f test %.2f barrier %.2f order %.2f (loads %.2f) apply %.2f barrier %.2f acct %.2f | records %.1f | order loop cycles %.0f\n",
+              h.dbg[0], h.dbg[1], h.dbg[1] / nb, h.dbg[2] / nb, h.dbg[3], h.dbg[4] / nb / 1e3, h.dbg[5] / nb / 1e3,
+              h.dbg[6] / nb / 1e3, h.dbg[7] / nb / 1e3, h.dbg[14] / nb / 1e3, h.dbg[8] / nb / 1e3, h.dbg[9] / nb / 1e3, h.dbg[10] / nb / 1e3,
+              h.dbg[11] / nb, h.dbg[15] / nb);
     }
     if (d_verify) {
       unsigned long long bad = 0;

@@ -1009,6 +1009,544 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// List mode, several commits per grid step (k_commit_lb).
+//
+// A list-mode step of k_commit is latency bound: one grid barrier, the
+// candidates' counts, the list test -- ~8 us for a few hundred new pairs, and
+// the 256x256 run has ~30 000 of them.  This kernel commits up to LB_M sources
+// per pair of grid barriers and stays exact:
+//
+//   select  every CTA derives, from the candidate set and the current counts,
+//           the LB_M + 1 smallest keys b_0 < b_1 < ... (48-bit key | pixel).
+//           The batch is the longest prefix whose trees are in the store; the
+//           next key (or the candidate threshold T) is the bound B: every
+//           pixel outside the batch has key >= B now and later (keys only
+//           grow).
+//   test    one pass over the unfilled-pair list tests each entry against the
+//           Euler intervals of all batch trees: J(e) = set of batch trees in
+//           which e is an ancestor pair.  Entries with J != 0 go to a hit
+//           buffer; entries with an endpoint in the batch whose count another
+//           batch tree would change go to a (small) record buffer.
+//   barrier
+//   order   every CTA replays the reference's selection on the records: take
+//           the least key among the remaining batch pixels (current counts);
+//           stop if it is not below B (an outside pixel may be next); commit
+//           it; every record it fills bumps the counts of its other batch
+//           endpoints.  This is FillingRateSelector.next_source
+//           (strategies.py:213-227) evaluated exactly, because the counts of
+//           the batch pixels after each commit are exactly what the records
+//           hold, and no outside pixel can undercut a key below B.
+//   apply   each hit is filled by the first committed tree of its J, in commit
+//           order (first writer wins, as in the sequential loop).
+//   barrier
+//
+// A record overflow commits b_0 alone (always valid).  Results equal the
+// one-commit-per-step loop bit for bit (tests/test_gpu_edge.py knob test).
+#ifndef GP_LB_M
+#define GP_LB_M 16
+#endif
+constexpr int LB_M = GP_LB_M;
+constexpr int LB_RPL = 4;             // records per lane of the ordering warp
+constexpr int LB_RCAP = 32 * LB_RPL;  // more records: the batch commits b_0 alone
+static_assert(LB_M == 4 || LB_M == 8 || LB_M == 16, "batch bits fit 16 bits; tinB rows are uint4s");
+constexpr int LB_H = LB_M < 8 ? LB_M : 8;  // trees tested per round of loads
+
+__device__ __forceinline__ int key_count(int strategy, unsigned key) {
+  return strategy == kExtrema ? (int)(key & 0xFFFFu) : (int)(key >> 16);
+}
+
+#define GP_CK(x) asm volatile("mov.u64 %0, %%clock64;" : "=l"(x)::"memory")
+template <int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_commit_lb(CommitArgs a) {
+  static_assert(THREADS >= CAND_CAP, "one candidate per thread");
+  __shared__ unsigned long long red64[32];
+  __shared__ uint32_t cand_s[CAND_CAP];
+  __shared__ unsigned wl_hi[CAND_CAP], wl_lo[CAND_CAP];  // per-warp sorted candidate keys
+  __shared__ unsigned cand_n, cand_T, cand_delta, cur_key;
+  __shared__ unsigned bhi[LB_M + 1], blo[LB_M + 1];
+  __shared__ int bslot[LB_M], bpix[LB_M], scnt[LB_M], cpix[LB_M];
+  __shared__ unsigned bstat[LB_M];
+  __shared__ int s_mb;
+  __shared__ unsigned s_T;  // key threshold of this batch: cand_T, or b_0 + 1 without a candidate set
+  __shared__ unsigned long long s_B;
+  __shared__ unsigned newc[LB_M];
+  __shared__ unsigned s_dead, s_sum, s_nh;
+  __shared__ unsigned char s_ordv[LB_M], s_posv[LB_M];  // tree at commit position f / position of tree t (0xFF: none)
+  __shared__ int s_mc;
+  if (a.ctl->status == CTL_DONE) return;
+  if (a.ctl->mode != 1) return;
+  const int N = a.g.N;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int gtid = blockIdx.x * blockDim.x + tid;
+  const bool keeper = gtid == 0;
+  const unsigned stride = gridDim.x * blockDim.x;
+  const MarkLayout L = a.L;
+  unsigned gen = ld_relaxed_gpu(&a.bar->gen);
+  int step = a.ctl->step;
+  unsigned lcur = __ldcg(&a.ctl->list_cur);
+  unsigned ln = __ldcg(&a.ctl->list_n[lcur]);
+  unsigned long long filled = 0, visits = 0;
+  if (keeper) {
+    filled = a.ctl->filled;
+    visits = a.ctl->visits;
+    a.ctl->cand_cnt[0] = a.ctl->cand_cnt[1] = a.ctl->cand_cnt[2] = 0;
+    a.lb->hit_n[0] = a.lb->hit_n[1] = 0;
+    a.lb->rec_n[0] = a.lb->rec_n[1] = 0;
+  }
+  if (tid == 0) {
+    cand_delta = max(1u, __ldcg(&a.ctl->cand_delta));
+    cand_n = 0;
+    cand_T = 0;
+    const unsigned long long sk0 = __ldcg(&a.selkey[step]);
+    cur_key = sk0 == ~0ull ? 0u : (unsigned)(sk0 >> 32);
+    s_dead = __ldcg(&a.ctl->list_dead);
+  }
+  if (tid < LB_M) newc[tid] = 0;
+  int status = CTL_RUNNING;
+  int cur_src = a.ctl->cur_src;
+  if (cur_src == -2) return;  // nothing left (the previous launch ended the run)
+  grid_barrier(a.bar, gen);  // counters zeroed; also orders the shared-memory initialisation
+  int done_here = 0;
+  unsigned ncollect = 0, nbatch = 0;
+  int mlim = LB_M;  // adaptive batch length
+  const bool dbgk = keeper && a.lb_debug;
+  unsigned long long tq[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (;;) {
+    // ---- candidates (grid-wide collection when the set is exhausted) ----
+    bool single = false;
+    if (dbgk) tq[0] = gtimer();
+    if (cand_n == 0) {
+      const unsigned candT_new = (((cur_key >> 16) + cand_delta) << 16);
+      const unsigned ci = ncollect % 3u;
+      if (keeper) a.ctl->cand_cnt[(ncollect + 1) % 3u] = 0;  // last read before the previous barrier
+      __syncthreads();  // every thread has read cand_n
+      {  // select_collect on counter ci
+        unsigned long long m = ~0ull;
+        for (int v0 = blockIdx.x * blockDim.x + (tid & ~31); v0 < N; v0 += (int)stride) {
+          const int v = v0 + lane;
+          unsigned key = 0xFFFFFFFFu;
+          if (v < N) {
+            key = sel_key(a.strategy, N, v, __ldcg(&a.cnt[v]), a.rank);
+            if (key != 0xFFFFFFFFu) m = min(m, sel_pack(key, v, __ldcg(&a.slot_of[v])));
+          }
+          const bool in = key < candT_new;
+          const unsigned bm = __ballot_sync(0xffffffffu, in);
+          if (bm) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(&a.ctl->cand_cnt[ci], (unsigned)__popc(bm));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const unsigned pos = base + __popc(bm & ((1u << lane) - 1u));
+            if (in && pos < (unsigned)CAND_CAP) a.cand[pos] = (uint32_t)v | (key_static(a.strategy, key) << 16);
+          }
+        }
+        m = block_reduce_min(m, red64);
+        if (tid == 0 && m != ~0ull) atomicMin(&a.selkey[step], m);
+      }
+      grid_barrier(a.bar, gen);
+      ncollect++;
+      if (dbgk) a.lb->dbg[3]++;
+      const unsigned long long sk = __ldcg(&a.selkey[step]);
+      if (sk == ~0ull) { status = CTL_DONE; cur_src = -2; break; }
+      const unsigned n = __ldcg(&a.ctl->cand_cnt[ci]);
+      const unsigned nv = (n > 0 && n <= (unsigned)CAND_CAP) ? n : 0u;
+      for (unsigned i = tid; i < nv; i += blockDim.x) cand_s[i] = __ldcg(&a.cand[i]);
+      __syncthreads();
+      if (tid == 0) {
+        cand_n = nv;
+        cand_T = candT_new;
+        cur_key = (unsigned)(sk >> 32);
+        if (n > (unsigned)CAND_CAP) cand_delta = max(1u, cand_delta >> 1);
+        else if (n < (unsigned)CAND_CAP / GP_CAND_GROW) cand_delta = min(cand_delta << 1, 4096u);
+      }
+      __syncthreads();
+      single = nv == 0;
+      if (single && tid == 0) {
+        // no usable set (more than CAND_CAP keys below the threshold, or none):
+        // this step commits the grid-wide minimum alone, as k_commit's slow path
+        bhi[0] = (unsigned)(sk >> 32);
+        blo[0] = (unsigned)sk;
+        for (int r = 1; r <= LB_M; r++) bhi[r] = blo[r] = 0xFFFFFFFFu;
+        s_T = bhi[0] + 1u;
+      }
+      if (single) __syncthreads();
+    }
+    // ---- the mlim + 1 smallest current keys of the set: every warp sorts its
+    // 32 candidates (bitonic, shuffles), warp 0 merges the sorted runs ----
+    if (!single) {
+      const unsigned cn = cand_n;
+      if (tid < CAND_CAP && (unsigned)(tid & ~31) < cn) {  // warps holding candidates
+        unsigned hi = 0xFFFFFFFFu, lo = 0xFFFFFFFFu;
+        if ((unsigned)tid < cn) {
+          const uint32_t e = cand_s[tid];
+          const int v = (int)(e & 0xFFFFu);
+          const int c = __ldcg(&a.cnt[v]);
+          const int sl = __ldcg(&a.slot_of[v]);
+          if (c < N - 1) {
+            hi = key_with_count(a.strategy, e >> 16, c);
+            lo = ((unsigned)v << 16) | (sl >= 0 && sl < 0xFFFF ? (unsigned)(sl + 1) : 0u);
+          }
+        }
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+          for (int j = k >> 1; j > 0; j >>= 1) {
+            const unsigned ph = __shfl_xor_sync(0xffffffffu, hi, j), pl = __shfl_xor_sync(0xffffffffu, lo, j);
+            const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+            const bool pless = ph < hi || (ph == hi && pl < lo);
+            const bool pmore = ph > hi || (ph == hi && pl > lo);
+            if ((lower == up) ? pless : pmore) { hi = ph; lo = pl; }
+          }
+        }
+        wl_hi[tid] = hi;
+        wl_lo[tid] = lo;
+      }
+      __syncthreads();
+      if (wid == 0) {
+        const unsigned nruns = (cn + 31u) >> 5;  // <= 16
+        unsigned head = 0;
+        unsigned kh = 0xFFFFFFFFu, kl = 0xFFFFFFFFu;
+        if ((unsigned)lane < nruns) { kh = wl_hi[lane * 32]; kl = wl_lo[lane * 32]; }
+#pragma unroll 1
+        for (int r = 0; r <= LB_M; r++) {
+          unsigned gh = 0xFFFFFFFFu, gl = 0xFFFFFFFFu;
+          if (r <= mlim) {
+            gh = __reduce_min_sync(0xffffffffu, kh);
+            gl = __reduce_min_sync(0xffffffffu, kh == gh ? kl : 0xFFFFFFFFu);
+            if (gh != 0xFFFFFFFFu && kh == gh && kl == gl) {  // the owner run advances
+              head++;
+              kh = kl = 0xFFFFFFFFu;
+              if (head < 32u) { kh = wl_hi[lane * 32 + head]; kl = wl_lo[lane * 32 + head]; }
+            }
+          }
+          if (lane == 0) { bhi[r] = gh; blo[r] = gl; }
+        }
+        if (lane == 0) s_T = cand_T;
+      }
+      __syncthreads();
+    }
+    if (bhi[0] == 0xFFFFFFFFu || bhi[0] >= s_T) {  // set exhausted: collect again
+      __syncthreads();
+      if (tid == 0) cand_n = 0;
+      __syncthreads();
+      continue;
+    }
+    // bhi[0] is the next source of the reference's loop
+    if (tid < LB_M) {
+      const int t = tid;
+      int sl = -1, px = -1;
+      if (bhi[t] < s_T) {
+        px = (int)(blo[t] >> 16);
+        sl = (int)(blo[t] & 0xFFFFu) - 1;
+        if (sl < 0) sl = __ldcg(&a.slot_of[px]);  // not encodable / no tree yet
+      }
+      bslot[t] = sl;
+      bpix[t] = px;
+      bstat[t] = key_static(a.strategy, bhi[t]);
+      scnt[t] = key_count(a.strategy, bhi[t]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int mb = 0;
+      const int room = min(mlim, a.max_steps - done_here);
+      while (mb < LB_M && mb < room && bhi[mb] < s_T && bslot[mb] >= 0) mb++;
+      s_mb = mb;
+      s_B = bhi[mb] < s_T ? (((unsigned long long)bhi[mb] << 16) | (blo[mb] >> 16))
+                          : ((unsigned long long)s_T << 16);
+      cur_key = bhi[0];
+    }
+    __syncthreads();
+    const int mb = s_mb;
+    if (mb == 0) {
+      status = done_here >= a.max_steps ? CTL_LIMIT : CTL_MISS;
+      cur_src = (int)(blo[0] >> 16);
+      if (keeper) atomicMin(&a.selkey[step], ((unsigned long long)bhi[0] << 32) | (blo[0] & 0xFFFF0000u));
+      break;
+    }
+    const unsigned par = nbatch & 1u;
+    if (dbgk) tq[1] = gtimer();
+    // ---- test: every list entry against the batch trees ----
+    // Long lists: the batch's Euler words are first transposed to pixel-major
+    // (tinB[x][t]: one or two 32-byte sectors per pixel), so an entry costs
+    // a few sectors per end instead of one per end and tree (the test is
+    // bound by L1/L2 sector throughput: ncu, profiles/).  One more grid
+    // barrier; short lists gather from the trees directly.
+    const bool packed = a.lb_tinb != nullptr && ln >= a.lb_pack_min;
+    constexpr int Q = LB_M / 4;  // uint4 per pixel
+    if (packed) {
+      const uint32_t* tin = a.ts.tin;
+      for (unsigned k = (unsigned)gtid; k < (unsigned)N * Q; k += stride) {
+        const unsigned x = k / Q, q = k % Q;
+        uint32_t z[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const int t = (int)q * 4 + j;
+          z[j] = t < mb ? __ldg(&tin[(unsigned)bslot[t] * (unsigned)N + x]) : 0u;
+        }
+        reinterpret_cast<uint4*>(a.lb_tinb)[k] = make_uint4(z[0], z[1], z[2], z[3]);
+      }
+      grid_barrier(a.bar, gen);
+    }
+    {
+      uint32_t* list = a.plist[lcur];
+      unsigned long long* hits = a.lb_hits;
+      const uint32_t* tin = a.ts.tin;
+      const uint4* tb = reinterpret_cast<const uint4*>(a.lb_tinb);
+      for (unsigned i0 = blockIdx.x * blockDim.x + (tid & ~31u); i0 < ln; i0 += stride) {
+        const unsigned i = i0 + lane;
+        const uint32_t e = i < ln ? __ldcg(&list[i]) : LIST_DEAD;
+        unsigned J = 0;
+        if (e != LIST_DEAD) {
+          const unsigned u = e >> 16, w = e & 0xFFFFu;
+#pragma unroll
+          for (int h0 = 0; h0 < LB_M; h0 += LB_H) {
+            if (h0 >= mb) break;
+            uint32_t zu[LB_H], zw[LB_H];
+            if (packed) {
+#pragma unroll
+              for (int q = 0; q < LB_H / 4; q++) {
+                const uint4 vu = __ldcg(&tb[u * Q + h0 / 4 + q]), vw = __ldcg(&tb[w * Q + h0 / 4 + q]);
+                zu[4 * q] = vu.x; zu[4 * q + 1] = vu.y; zu[4 * q + 2] = vu.z; zu[4 * q + 3] = vu.w;
+                zw[4 * q] = vw.x; zw[4 * q + 1] = vw.y; zw[4 * q + 2] = vw.z; zw[4 * q + 3] = vw.w;
+              }
+            } else {
+#pragma unroll
+              for (int t = 0; t < LB_H; t++) {
+                zu[t] = zw[t] = 0u;
+                if (h0 + t < mb) {
+                  const unsigned toff = (unsigned)bslot[h0 + t] * (unsigned)N;  // fits 32 bits
+                  zu[t] = __ldg(&tin[toff + u]);
+                  zw[t] = __ldg(&tin[toff + w]);
+                }
+              }
+            }
+#pragma unroll
+            for (int t = 0; t < LB_H; t++) {
+              // positions mod 2^16: exact, a subtree ends at or before position N - 1
+              const unsigned d = zw[t] - zu[t];
+              const bool hit = ((d - 1u) & 0xFFFFu) < (zu[t] >> 16) || (~d & 0xFFFFu) < (zw[t] >> 16);
+              J |= (unsigned)hit << (h0 + t);
+            }
+          }
+        }
+        const unsigned hm = __ballot_sync(0xffffffffu, J != 0);
+        if (hm) {
+          unsigned base = 0;
+          if (lane == 0) base = atomicAdd(&a.lb->hit_n[par], (unsigned)__popc(hm));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (J) {
+            hits[base + __popc(hm & ((1u << lane) - 1u))] = ((unsigned long long)i << 16) | J;
+            // records: an endpoint in the batch whose count another batch tree changes
+            const int u = (int)(e >> 16), w = (int)(e & 0xFFFFu);
+            unsigned iu = 0xFFu, iw = 0xFFu;
+            for (int t = 0; t < mb; t++) {
+              if (u == bpix[t]) iu = (unsigned)t;
+              if (w == bpix[t]) iw = (unsigned)t;
+            }
+            if ((iu != 0xFFu && (J & ~(1u << iu))) || (iw != 0xFFu && (J & ~(1u << iw)))) {
+              const unsigned r = atomicAdd(&a.lb->rec_n[par], 1u);
+              if (r < (unsigned)LB_RCAP) a.lb->recs[r] = J | (iu << 16) | (iw << 24);
+            }
+          }
+        }
+      }
+    }
+    if (dbgk) tq[2] = gtimer();
+    grid_barrier(a.bar, gen);
+    if (dbgk) tq[3] = gtimer();
+    // ---- order: the reference's selection replayed on the records (warp 0) ----
+    if (keeper) {  // the other parity's counters: last read before the previous barrier
+      a.lb->hit_n[par ^ 1u] = 0;
+      a.lb->rec_n[par ^ 1u] = 0;
+    }
+    unsigned nrec = 0;
+    bool over = false;
+    if (wid == 0) {
+      // Everything in registers: lane t owns batch pixel t (its count, its
+      // commit position), lane r owns records r, r + 32, ... (LB_RPL each).
+      unsigned v = 0;  // one load per CTA of each counter
+      if (lane == 0) v = __ldcg(&a.lb->rec_n[par]);
+      if (lane == 1) v = __ldcg(&a.lb->hit_n[par]);
+      nrec = __shfl_sync(0xffffffffu, v, 0);
+      if (lane == 1) s_nh = v;
+      over = nrec > (unsigned)LB_RCAP;
+      uint32_t rec[LB_RPL];
+#pragma unroll
+      for (int k = 0; k < LB_RPL; k++) {
+        const unsigned i = (unsigned)(k * 32 + lane);
+        rec[k] = (!over && i < nrec) ? __ldcg(&a.lb->recs[i]) : 0u;
+      }
+      if (dbgk) tq[7] = gtimer();
+      long long kc2, kc3;
+      GP_CK(kc2);
+      int m = 0;
+      const unsigned long long B = s_B;
+      const unsigned mystat = lane < mb ? bstat[lane] : 0u;
+      const unsigned mypix = lane < mb ? (unsigned)bpix[lane] : 0xFFFFFFFFu;
+      int mycnt = lane < mb ? scnt[lane] : N;
+      bool alive = lane < mb;
+      unsigned mypos = 0xFFu, myord = 0xFFu;
+      // (the warp must enter the loop converged: diverged, every redux / vote
+      // below takes the slow collective path and the loop runs ~4x longer)
+      __syncwarp();
+      for (int it = 0; it < mb; it++) {
+        const unsigned kh = (alive && mycnt < N - 1) ? key_with_count(a.strategy, mystat, mycnt) : 0xFFFFFFFFu;
+        const unsigned gh = __reduce_min_sync(0xffffffffu, kh);
+        if (gh == 0xFFFFFFFFu) break;
+        const unsigned gl = __reduce_min_sync(0xffffffffu, kh == gh ? mypix : 0xFFFFFFFFu);
+        if ((((unsigned long long)gh << 16) | gl) >= B) break;
+        const bool me = kh == gh && mypix == gl;
+        const int best = __ffs(__ballot_sync(0xffffffffu, me)) - 1;
+        if (me) { alive = false; mypos = (unsigned)m; }
+        if (lane == m) myord = (unsigned)best;
+        m++;
+        if (over || it == mb - 1) break;
+        // records this commit fills: their other batch endpoints gain one pair
+#pragma unroll
+        for (int k = 0; k < LB_RPL; k++) {
+          const bool hitr = (rec[k] >> best) & 1u;
+          unsigned hm = __ballot_sync(0xffffffffu, hitr);
+          const unsigned t1 = (rec[k] >> 16) & 0xFFu, t2 = rec[k] >> 24;
+          if (hitr) rec[k] &= 0xFFFF0000u;  // filled
+          while (hm) {
+            const int src = __ffs(hm) - 1;
+            hm &= hm - 1;
+            const unsigned a1 = __shfl_sync(0xffffffffu, t1, src), a2 = __shfl_sync(0xffffffffu, t2, src);
+            mycnt += (a1 == (unsigned)lane && a1 != (unsigned)best) + (a2 == (unsigned)lane && a2 != (unsigned)best);
+          }
+        }
+      }
+      GP_CK(kc3);
+      if (dbgk) a.lb->dbg[15] += (unsigned long long)(kc3 - kc2);
+      if (lane < LB_M) s_posv[lane] = (unsigned char)mypos;
+      if (lane < m) {
+        s_ordv[lane] = (unsigned char)myord;
+        cpix[lane] = bpix[myord];
+      }
+      if (lane == 0) s_mc = m;
+    }
+    __syncthreads();
+    const int mc = s_mc;
+    const unsigned nh = s_nh;
+    // (mc >= 1: b_0 is below B by construction)
+    if (dbgk) tq[4] = gtimer();
+    // ---- apply: each hit is filled by the first committed tree of its J ----
+    {
+      uint32_t* list = a.plist[lcur];
+      const unsigned long long* hits = a.lb_hits;
+      for (unsigned h = (unsigned)gtid; h < nh; h += stride) {
+        const unsigned long long hv = __ldcg(&hits[h]);
+        unsigned J = (unsigned)hv & 0xFFFFu, f = 0xFFu;
+        while (J) {
+          const int t = __ffs(J) - 1;
+          J &= J - 1;
+          f = min(f, (unsigned)s_posv[t]);
+        }
+        if (f == 0xFFu) continue;  // its trees were not committed in this batch
+        const int t = (int)s_ordv[f];
+        const unsigned i = (unsigned)(hv >> 16);
+        const uint32_t e = __ldcg(&list[i]);
+        const size_t toff = (size_t)bslot[t] * N;
+        const uint32_t* tinz = a.ts.tin + toff;
+        const uint32_t zu = __ldg(&tinz[e >> 16]), zw = __ldg(&tinz[e & 0xFFFFu]);
+        const unsigned tu = zu & 0xFFFFu, tw = zw & 0xFFFFu;
+        const bool uw = tw - tu - 1u < (zu >> 16);
+        const int anc = uw ? (int)(e >> 16) : (int)(e & 0xFFFFu);
+        const int des = uw ? (int)(e & 0xFFFFu) : (int)(e >> 16);
+        const unsigned ta = uw ? tu : tw, td = uw ? tw : tu;
+        const uint32_t ca = mcol(L, (uint32_t)anc), cd = mcol(L, (uint32_t)des);
+        atomicOr(&a.mark[mword(L, (uint32_t)anc, cd)], 1u << (cd & 31));
+        atomicOr(&a.mark[mword(L, (uint32_t)des, ca)], 1u << (ca & 31));
+        const float* tdp = a.ts.tdp + toff;
+        const float duv = __fsub_rn(__ldg(&tdp[td]), __ldg(&tdp[ta]));
+        a.D[(size_t)anc * N + des] = duv;
+        a.D[(size_t)des * N + anc] = duv;
+        // committed roots end the batch full (count N-1, set by the keeper)
+        bool ra = false, rd = false;
+        for (int k = 0; k < mc; k++) {
+          ra |= cpix[k] == anc;
+          rd |= cpix[k] == des;
+        }
+        if (!ra) atomicAdd(&a.cnt[anc], 1);
+        if (!rd) atomicAdd(&a.cnt[des], 1);
+        list[i] = LIST_DEAD;
+        atomicAdd(&newc[f], 1u);
+      }
+    }
+    __syncthreads();
+    if (tid < mc && newc[tid]) atomicAdd(&a.newp[step + tid], (unsigned long long)newc[tid]);
+    if (tid < LB_M) newc[tid] = 0;
+    if (blockIdx.x == 0 && wid == 0) {
+      unsigned cv = 0;
+      if (lane < mc) {
+        const int px = cpix[lane];
+        a.cnt[px] = N - 1;  // the root pairs with every pixel
+        a.seq[step + lane] = px;
+        a.slot_of[px] = -2;  // committed
+        cv = __ldg(&a.ts.C[bslot[s_ordv[lane]]]);
+      }
+      unsigned long long cs = cv;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+      if (lane == 0) visits += cs;
+    }
+    if (dbgk) tq[5] = gtimer();
+    grid_barrier(a.bar, gen);
+    if (dbgk) tq[6] = gtimer();
+    // ---- accounting (every CTA keeps the dead count: uniform compaction decisions) ----
+    if (wid == 0) {
+      unsigned sum = lane < mc ? (unsigned)__ldcg(&a.newp[step + lane]) : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) {
+        s_sum = sum;
+        s_dead += sum;
+      }
+    }
+    __syncthreads();
+    if (keeper) filled += s_sum;
+    step += mc;
+    done_here += mc;
+    nbatch++;
+    mlim = mc < mb ? max(1, mc) : min(LB_M, mlim * 2);
+    if (dbgk) {
+      unsigned long long* d = a.lb->dbg;
+      d[0]++;
+      d[1] += mc;
+      d[2] += mb;
+      d[4] += tq[1] - tq[0];
+      d[5] += tq[2] - tq[1];
+      d[6] += tq[3] - tq[2];
+      d[7] += tq[4] - tq[3];
+      d[8] += tq[5] - tq[4];
+      d[9] += tq[6] - tq[5];
+      d[10] += gtimer() - tq[6];
+      d[11] += nrec;
+      d[14] += tq[7] - tq[3];
+    }
+    if ((unsigned long long)s_dead * a.compact_div > ln && ln) {  // compaction (uniform)
+      compact_list(a, lcur, ln);
+      grid_barrier(a.bar, gen);
+      if (keeper) a.ctl->list_n[lcur] = 0;
+      lcur ^= 1u;
+      ln = __ldcg(&a.ctl->list_n[lcur]);
+      __syncthreads();
+      if (tid == 0) s_dead = 0;
+      __syncthreads();
+    }
+  }
+  if (keeper) {
+    a.ctl->step = step;
+    a.ctl->cur_src = cur_src;
+    a.ctl->status = status;
+    a.ctl->filled = filled;
+    a.ctl->visits = visits;
+    a.ctl->list_dead = s_dead;
+    a.ctl->list_cur = lcur;
+    a.ctl->cand_delta = cand_delta;
+  }
+}
+
 // Fill pipelining depth G (chunk descriptors in flight per warp, default 4).
 // CTA shape of the commit kernel, chosen per run (commit_configure): one
 // 1024-thread CTA per SM for large maps (fewer, larger CTA queues; cheaper
@@ -1099,6 +1637,27 @@ bool commit_split() {
   return v != 0 && (commit_threads() == 1024 || commit_fill_depth() == 4);
 }
 
+// batched list-mode kernel (k_commit_lb), same shapes as list_kernel()
+static const void* lb_kernel() {
+  if (commit_threads() != 1024) return (const void*)k_commit_lb<512, 2>;
+  return list_cfg() == 1 ? (const void*)k_commit_lb<1024, 2>
+       : list_cfg() == 2 ? (const void*)k_commit_lb<512, 2> : (const void*)k_commit_lb<1024, 1>;
+}
+
+static int lb_blocks() {
+  static int nb[2][3] = {};
+  const int k = commit_threads() == 1024 ? 1 : 0, lc = list_cfg();
+  int* cached = &nb[k][lc];
+  if (!*cached) {
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lb_kernel(), list_threads(), 0);
+    *cached = nsm * std::max(1, std::min(per_sm, (k && lc == 0) ? 1 : 2));
+  }
+  return *cached;
+}
+
 cudaError_t launch_commit_split(const CommitArgs& a, int num_blocks, cudaStream_t st) {
   CommitArgs args = a;
   void* params[] = {&args};
@@ -1106,6 +1665,8 @@ cudaError_t launch_commit_split(const CommitArgs& a, int num_blocks, cudaStream_
                                             : (const void*)k_commit<4, 512, 2, 0>;
   cudaError_t e = cudaLaunchCooperativeKernel(tk, dim3(num_blocks), dim3(commit_threads()), params, 0, st);
   if (e != cudaSuccess) return e;
+  if (a.lb && a.cand && a.strategy != kNaive)
+    return cudaLaunchCooperativeKernel(lb_kernel(), dim3(lb_blocks()), dim3(list_threads()), params, 0, st);
   return cudaLaunchCooperativeKernel(list_kernel(), dim3(list_blocks()), dim3(list_threads()), params, 0, st);
 }
 

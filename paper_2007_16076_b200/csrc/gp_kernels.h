@@ -96,8 +96,7 @@ struct Ctl {
   unsigned long long list_switch;  // switch to list mode when unfilled <= this
   int build;                       // list build pending (set by k_switch_prep)
   unsigned cand_delta;             // candidate-set width in counts (k_commit, adaptive)
-  unsigned cand_cnt[2];            // candidate collection counters (step parity)
-  unsigned pad4;
+  unsigned cand_cnt[3];            // candidate collection counters (k_commit: step parity; k_commit_lb: rotating)
 };
 enum { CTL_RUNNING = 0, CTL_DONE = 1, CTL_MISS = 2, CTL_LIMIT = 3, CTL_SWITCH = 4 };
 
@@ -107,6 +106,14 @@ struct GridBarrier {
   unsigned pad0[31];
   unsigned gen;
   unsigned pad1[31];
+};
+
+// batched list-mode commits (k_commit_lb): hit / record counters by batch parity, records
+struct LbCtl {
+  unsigned hit_n[2];
+  unsigned rec_n[2];
+  uint32_t recs[2048];  // J | endpoint batch indices << 16 / << 24 (0xFF: none)
+  unsigned long long dbg[16];  // GP_LB_DEBUG: batches, commits, batch sizes, collects, phase ns sums
 };
 
 struct CommitArgs {
@@ -136,6 +143,11 @@ struct CommitArgs {
   unsigned long long* dbgo; // optional per-step open-pixel counts (debug dump)
   GridBarrier* bar;
   uint32_t* plist[2];      // unfilled pairs (u << 16 | w, u < w), list mode
+  LbCtl* lb;               // batched list-mode commits (nullptr: one commit per step)
+  unsigned long long* lb_hits;  // [list capacity] entry index << 16 | J
+  int lb_debug;            // GP_LB_DEBUG: phase time sums in lb->dbg
+  uint32_t* lb_tinb;       // [N][LB_M] pixel-major Euler words of the batch trees (nullptr: off)
+  unsigned lb_pack_min;    // least list length that pays for the transposition
   uint32_t* cand;          // [CAND_CAP] candidate set (pixel | rank << 16); nullptr: off
   unsigned compact_div;    // list mode: compact when dead entries > live / compact_div
   int lpt;                 // top-K: candidates deepest-first (longest trees first in the batch)
