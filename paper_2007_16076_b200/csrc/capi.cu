@@ -1008,7 +1008,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     {
       // measured: 256^2 flat in [1, 1.5]; 128^2 best at 3-5; 64^2 at 10
       // (1 for tiny test images, which then exercise the tree fill too)
-      double alpha = N >= 32768 ? 1.0 : N > 8192 ? 3.0 : N > 1024 ? 10.0 : 1.0;
+      double alpha = N >= 32768 ? 1.5 : N > 8192 ? 3.0 : N > 1024 ? 10.0 : 1.0;
       if (const char* e = getenv("GP_LIST_ALPHA")) alpha = atof(e);
       const double est_tree = (double)N * std::sqrt((double)N) * 0.5;
       double sw = alpha * est_tree;
@@ -1187,8 +1187,11 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       ca.plist[0] = c->list[0];
       ca.plist[1] = c->list[1];
       // list mode: several commits per grid step (k_commit_lb); GP_LIST_BATCH=0: one per step
-      if (ca.cand && ca.strategy != kNaive && commit_split() &&
-          !(getenv("GP_LIST_BATCH") && !atoi(getenv("GP_LIST_BATCH")))) {
+      // (measured: 256^2 list phase 257 -> 140 ms, 128^2 configs -4 ms; 64^2
+      // loses -- 2 commits per batch against the batch's two barriers -- so
+      // maps below 8192 pixels keep the one-commit steps unless forced)
+      const bool lb_on = getenv("GP_LIST_BATCH") ? atoi(getenv("GP_LIST_BATCH")) != 0 : N >= 8192;
+      if (ca.cand && ca.strategy != kNaive && commit_split() && lb_on) {
         LbCtl* d_lb = nullptr;
         unsigned long long* d_hits = nullptr;
         CUDA_TRY(ws_get(c, WS_LB, &d_lb, 1));
@@ -1197,6 +1200,8 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
         ca.lb = d_lb;
         ca.lb_hits = d_hits;
         ca.lb_debug = getenv("GP_LB_DEBUG") && atoi(getenv("GP_LB_DEBUG"));
+        ca.lb_rcap = 1u << 30;  // GP_LB_RCAP (tests): records above it take the overflow path
+        if (const char* e = getenv("GP_LB_RCAP")) ca.lb_rcap = (unsigned)std::max(0, atoi(e));
         ca.lb_pack_min = 65536;
         if (const char* e = getenv("GP_LB_PACK_MIN")) ca.lb_pack_min = (unsigned)std::max(0, atoi(e));
         if (!(getenv("GP_LB_PACK") && !atoi(getenv("GP_LB_PACK")))) {

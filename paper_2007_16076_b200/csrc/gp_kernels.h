@@ -148,6 +148,7 @@ struct CommitArgs {
   int lb_debug;            // GP_LB_DEBUG: phase time sums in lb->dbg
   uint32_t* lb_tinb;       // [N][LB_M] pixel-major Euler words of the batch trees (nullptr: off)
   unsigned lb_pack_min;    // least list length that pays for the transposition
+  unsigned lb_rcap;        // records a batch may hold (<= 128; above: the batch commits its first source alone)
   uint32_t* cand;          // [CAND_CAP] candidate set (pixel | rank << 16); nullptr: off
   unsigned compact_div;    // list mode: compact when dead entries > live / compact_div
   int lpt;                 // top-K: candidates deepest-first (longest trees first in the batch)

@@ -116,6 +116,13 @@ def test_fp32_zero_pixels_exact_heap(gp, oracle):
     {"GP_PROP_CLUSTER": "2"}, {"GP_PROP_CLUSTER": "2", "GP_LIST_ALPHA": "1000"}, {"GP_VERIFY": "1"},
     {"GP_CAND": "0"}, {"GP_LPT": "0"}, {"GP_COMMIT_SPLIT": "0"}, {"GP_LIST_CFG": "2"}, {"GP_LIST_CFG": "1"}, {"GP_PROP_LEAN": "0"}, {"GP_PROP_MC": "0"},
     {"GP_COMPACT_DIV": "1"}, {"GP_COMPACT_DIV": "64"}, {"GP_LIST_ALPHA": "1", "GP_COMPACT_DIV": "1"},
+    # batched list-mode commits (k_commit_lb): forced on this small map, packed / direct test,
+    # record overflow path, longer list phases, one commit per step
+    {"GP_LIST_BATCH": "1"}, {"GP_LIST_BATCH": "1", "GP_LB_PACK_MIN": "0"}, {"GP_LIST_BATCH": "1", "GP_LB_PACK": "0"},
+    {"GP_LIST_BATCH": "1", "GP_LB_RCAP": "0"}, {"GP_LIST_BATCH": "1", "GP_LB_RCAP": "3", "GP_LB_PACK_MIN": "0"},
+    {"GP_LIST_BATCH": "1", "GP_LIST_ALPHA": "6"}, {"GP_LIST_BATCH": "1", "GP_LIST_ALPHA": "6", "GP_LB_PACK_MIN": "0"},
+    {"GP_LIST_BATCH": "1", "GP_COMPACT_DIV": "1"}, {"GP_LIST_BATCH": "1", "GP_CAND": "0"},
+    {"GP_LIST_BATCH": "0"},
 ])
 def test_tuning_knobs_do_not_change_results(gp, oracle, env, monkeypatch):
     img = np.random.default_rng(11).random((24, 20), dtype=np.float32)
@@ -200,6 +207,33 @@ def test_run_loops_agree_on_a_larger_image(gp, oracle, pipeline, monkeypatch):
     run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, gp.StrategyKind.FILLING_RATE)
     assert _seq(run) == o["seq"].tolist()
     assert np.array_equal(run.distances.dist, o["D"])
+
+
+@pytest.mark.parametrize("kind", ["filling-rate", "extrema"])
+@pytest.mark.parametrize("isint", [True, False])
+def test_batched_list_commits_equal_single_commits(gp, kind, isint, monkeypatch):
+    """k_commit_lb (several commits per grid step, default above 8192 pixels) against the
+    one-commit-per-step list kernel on a 96x100 map: same sequence, same new pairs per
+    commit, same array -- for the filling-rate and the extrema keys (the configs' goldens pin
+    the filling-rate path to the reference / oracle)."""
+    rng = np.random.default_rng(33)
+    img = rng.integers(1, 256, (96, 100)) if isint else rng.random((96, 100), dtype=np.float32)
+    sk = gp.StrategyKind.FILLING_RATE if kind == "filling-rate" else gp.StrategyKind.EXTREMA
+    out = []
+    for env in ({"GP_LIST_BATCH": "0"}, {"GP_LIST_BATCH": "1"}, {"GP_LIST_BATCH": "1", "GP_LB_PACK_MIN": "0"},
+                {"GP_LIST_BATCH": "1", "GP_LB_RCAP": "2"}):
+        for k in ("GP_LIST_BATCH", "GP_LB_PACK_MIN", "GP_LB_RCAP"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        run = gp.run_strategy(gp.Image(img), gp.Metric.SUM, sk)
+        D = run.distances.dist
+        out.append((_seq(run), [c for _, _, c in run.trace.samples], hashlib.sha256(D.tobytes()).hexdigest()))
+        assert np.array_equal(D, D.T)
+    for o in out[1:]:
+        assert o[0] == out[0][0], "committed sequence differs"
+        assert o[1] == out[0][1], "per-commit fill counts differ"
+        assert o[2] == out[0][2], "distance array differs"
 
 
 def _check_tree(dist, parent, img, conn, metric, sources):
