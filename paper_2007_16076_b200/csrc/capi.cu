@@ -913,6 +913,17 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   CUDA_TRY(cudaEventRecord(tot.a, st));
   CUDA_TRY(cudaEventRecord(setup.a, st));
   CUDA_TRY(cudaMemsetAsync(s->cnt, 0, (size_t)N * 4, st));
+  // One-sided tree fills (device-resident result): D starts as the NaN
+  // sentinel, tree-mode fills store the ancestor's row only, and one
+  // transpose-merge pass after the run completes the symmetric array (saves
+  // the scattered mirrored store of every new pair; GP_ONE_SIDED=0 off).
+  // gp_run_to_host keeps two-sided fills: it streams complete rows as the run
+  // proceeds (completing rows from their mirrored elements just before the
+  // copy was measured slower: e2e 1.575 vs 1.496 s per 256^2 image).
+  const bool one_sided = !D_host && !(strategy == GP_STRATEGY_NAIVE && !naive_with_tree) &&
+                         !(getenv("GP_VERIFY") && atoi(getenv("GP_VERIFY"))) &&
+                         !(getenv("GP_ONE_SIDED") && !atoi(getenv("GP_ONE_SIDED")));
+  if (one_sided) CUDA_TRY(cudaMemsetAsync(s->D, 0xFF, (size_t)N * N * 4, st));
   CUDA_TRY(launch_store_init(L, s->mark, s->D, st));
   S.kernels += 1;
 
@@ -1085,6 +1096,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     ca.ext = d_ext;
     ca.selkey = d_selkey;
     ca.stepflags = d_flags;
+    ca.one_sided = one_sided ? 1 : 0;
     ca.seq = d_seq;
     ca.newp = d_new;
     ca.ctl = d_ctl;
@@ -1360,6 +1372,10 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       }
     }
     CUDA_TRY(cudaStreamSynchronize(ps));
+    if (one_sided) {
+      CUDA_TRY(launch_merge_sym(s->D, N, st));
+      S.kernels += 1;
+    }
     CUDA_TRY(cudaEventRecord(tot.b, st));
     CUDA_TRY(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     if (d_cen) {

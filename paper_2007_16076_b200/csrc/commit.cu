@@ -33,6 +33,7 @@
 // the store (the host then propagates a speculative batch: the top-K open
 // pixels by the same key, K1) or when the array is complete.  A tree depends
 // only on its source, so speculation never changes the committed sequence.
+#include <algorithm>
 #include <cooperative_groups.h>
 
 #include "gp_common.cuh"
@@ -287,7 +288,7 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
             float duv = __fsub_rn(__ldg(&tdp[qb + kb + 32u * j + lane]), __ldg(&tdp[qb - 1]));
             if (VERIFY && corrupt) duv = __fadd_rn(duv, 1.0f);  // verify test hook
             a.D[(size_t)u * N + w] = duv;
-            a.D[(size_t)w * N + u] = duv;
+            if (!a.one_sided) a.D[(size_t)w * N + u] = duv;
             atomicAdd(&a.cnt[w], 1);
             unew++;
           } else if (VERIFY && a.verify && kb + 32u * j + lane < kend) {
@@ -595,7 +596,7 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
           set_mark(a, w, ucol);
           const float duv = __fsub_rn(__ldg(&tdp[qb + c * 32u + lane]), __ldg(&tdp[qb - 1]));
           a.D[(size_t)u * N + w] = duv;
-          a.D[(size_t)w * N + u] = duv;
+          if (!a.one_sided) a.D[(size_t)w * N + u] = duv;
           atomicAdd(&a.cnt[w], 1);
         }
         if (lane == 0) {
@@ -644,7 +645,7 @@ __device__ __forceinline__ unsigned fill_root_row(const CommitArgs& a, int slot,
       set_mark(a, x, scol);
       const float d = __ldg(&tdp[__ldg(&tin[x]) & 0xFFFFu]);
       a.D[(size_t)s * N + x] = d;
-      a.D[(size_t)x * N + s] = d;
+      if (!a.one_sided) a.D[(size_t)x * N + s] = d;
       atomicAdd(&a.cnt[x], 1);
       mine++;
     }
@@ -1979,6 +1980,53 @@ __global__ void k_build_list_gated(MarkLayout L, const uint32_t* mark, uint32_t*
 cudaError_t launch_switch(const CommitArgs& a, uint32_t* list0, cudaStream_t st) {
   k_switch_prep<<<1, 32, 0, st>>>(a.ctl);
   k_build_list_gated<<<148 * 8, 256, 0, st>>>(a.L, a.mark, list0, a.ctl);
+  return cudaGetLastError();
+}
+
+// One-sided tree fills (CommitArgs::one_sided): during the run a new pair's
+// value is stored in the ancestor's row only, D[anc][des]; the mirrored
+// element keeps the store's NaN sentinel (all ones).  This pass completes the
+// symmetric array: for every tile pair (I, J), I <= J, each element takes
+// whichever of D[i][j], D[j][i] was written (list-mode fills write both).
+// It reads and writes D once (~24 GiB of HBM traffic at 256x256).
+__global__ void __launch_bounds__(256) k_merge_sym(float* D, int N, int T) {
+  __shared__ uint32_t ta[32][33], tb[32][33];
+  // tile pair index -> (I, J), I <= J
+  const long long p = blockIdx.x;
+  int I = (int)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
+  while ((long long)(I + 1) * (I + 2) / 2 <= p) I++;
+  while ((long long)I * (I + 1) / 2 > p) I--;
+  const int Jr = (int)(p - (long long)I * (I + 1) / 2);  // 0 .. I
+  // (I here counts the larger index; name the pair (r, c) with r <= c)
+  const int r0 = Jr * 32, c0 = I * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows per pass
+  uint32_t* Du = reinterpret_cast<uint32_t*>(D);
+  for (int y = ty; y < 32; y += 8) {
+    const int ra = r0 + y, ca = c0 + tx;  // A = D[r0.., c0..]
+    ta[y][tx] = (ra < N && ca < N) ? Du[(size_t)ra * N + ca] : 0xFFFFFFFFu;
+    const int rb = c0 + y, cb = r0 + tx;  // B = D[c0.., r0..]
+    tb[y][tx] = (rb < N && cb < N) ? Du[(size_t)rb * N + cb] : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    {
+      const int ra = r0 + y, ca = c0 + tx;
+      const uint32_t a = ta[y][tx], b = tb[tx][y];
+      if (ra < N && ca < N && a == 0xFFFFFFFFu && b != 0xFFFFFFFFu) Du[(size_t)ra * N + ca] = b;
+    }
+    if (r0 != c0) {
+      const int rb = c0 + y, cb = r0 + tx;
+      const uint32_t b = tb[y][tx], a = ta[tx][y];
+      if (rb < N && cb < N && b == 0xFFFFFFFFu && a != 0xFFFFFFFFu) Du[(size_t)rb * N + cb] = a;
+    }
+  }
+  (void)T;
+}
+
+cudaError_t launch_merge_sym(float* D, int N, cudaStream_t st) {
+  const long long T = (N + 31) / 32;
+  const long long pairs = T * (T + 1) / 2;
+  k_merge_sym<<<(unsigned)pairs, 256, 0, st>>>(D, N, (int)T);
   return cudaGetLastError();
 }
 

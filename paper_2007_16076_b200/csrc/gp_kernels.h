@@ -143,6 +143,7 @@ struct CommitArgs {
   unsigned long long* dbgo; // optional per-step open-pixel counts (debug dump)
   GridBarrier* bar;
   uint32_t* plist[2];      // unfilled pairs (u << 16 | w, u < w), list mode
+  int one_sided;           // tree fills store D[anc][des] only (launch_merge_sym completes D after the run)
   LbCtl* lb;               // batched list-mode commits (nullptr: one commit per step)
   unsigned long long* lb_hits;  // [list capacity] entry index << 16 | J
   int lb_debug;            // GP_LB_DEBUG: phase time sums in lb->dbg
@@ -177,6 +178,7 @@ cudaError_t launch_switch(const CommitArgs& a, uint32_t* list0, cudaStream_t st)
 
 // ---------------- store helpers ----------------
 cudaError_t launch_store_init(const MarkLayout& L, uint32_t* mark, float* D, cudaStream_t st);
+cudaError_t launch_merge_sym(float* D, int N, cudaStream_t st);
 // filling-rate ranking on the device (setup.cu): ext / rank from dist_from_c
 size_t ext_rank_temp_bytes(int N);
 cudaError_t launch_ext_rank(const float* dfc, int N, unsigned long long* keys2, void* temp,
