@@ -8,11 +8,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
+#include <utility>
 #include <vector>
 
 #include "../../include/geopairs_b200.h"
@@ -47,6 +50,7 @@ struct gp_ctx {
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;  // propagation stream of the host-driven (debug) loop
   cudaStream_t st3 = nullptr;  // device-to-host stream of completed D rows (gp_run_to_host)
+
   int border_n = -1;           // border source list resident in the workspace (its length)
   int* h_cnt = nullptr;        // pinned copy of the per-pixel counts
   int nsm = 148;
@@ -62,7 +66,11 @@ struct gp_ctx {
   unsigned char* big = nullptr;  // scratch of the whole-GPU K1 (contexts above 65 536 pixels)
   unsigned* h_flag = nullptr;    // pinned pass flag of the whole-GPU K1
   uint32_t* list[2] = {nullptr, nullptr};  // unfilled-pair lists (late phase)
-  int* h_cnt2 = nullptr;     // pinned: two count snapshots (host-row rounds)
+  int* h_cnt2 = nullptr;     // pinned: count snapshots of the host-row rounds (rotating)
+  int* d_stage_cnt = nullptr;  // device stage of the snapshots (copied out by a second stream)
+  Ctl* d_stage_ctl = nullptr;
+  cudaStream_t st4 = nullptr;  // snapshot copies
+  int* h_done = nullptr;       // mapped pinned: set by the commit kernel when the array is complete
   Ctl* h_ctl2 = nullptr;     // pinned: two control-block snapshots
   void* ws[32] = {};      // run workspace, cached across runs (no cudaMalloc in gp_run)
   size_t ws_bytes[32] = {};
@@ -231,8 +239,13 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
   if (c->st) cudaStreamDestroy(c->st);
   if (c->st2) cudaStreamDestroy(c->st2);
   if (c->st3) cudaStreamDestroy(c->st3);
+
   if (c->h_cnt) cudaFreeHost(c->h_cnt);
   if (c->h_cnt2) cudaFreeHost(c->h_cnt2);
+  cudaFree(c->d_stage_cnt);
+  cudaFree(c->d_stage_ctl);
+  if (c->st4) cudaStreamDestroy(c->st4);
+  if (c->h_done) cudaFreeHost(c->h_done);
   if (c->h_ctl2) cudaFreeHost(c->h_ctl2);
   delete c;
 }
@@ -241,7 +254,7 @@ extern "C" int gp_ctx_num_pixels(const gp_ctx* c) { return c ? c->g.N : 0; }
 
 enum { WS_SEQ, WS_NEW, WS_SRC, WS_SLOT_OF, WS_RANK, WS_EXT, WS_SELKEY, WS_FLAGS, WS_CTL, WS_DFC,
        WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK, WS_EXTK, WS_EXTT, WS_CSET,
-       WS_VERIFY, WS_CS_SRC, WS_CS_DIST, WS_CS_DIR, WS_CS_PAR, WS_LB, WS_LBHITS, WS_LBTINB };
+       WS_VERIFY, WS_CS_SRC, WS_CS_DIST, WS_CS_DIR, WS_CS_PAR, WS_LB, WS_LBHITS, WS_LBTINB, WS_PATCH };
 
 template <typename T>
 static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
@@ -831,6 +844,7 @@ struct RowStreamer {
   }
   ~RowStreamer() {
     if (snap_ev) cudaEventDestroy(snap_ev);
+    for (cudaEvent_t e : fence) if (e) cudaEventDestroy(e);
   }
   int enqueue(bool all, bool read = true, const int* cnt = nullptr) {
     const int N = c->g.N;
@@ -845,18 +859,51 @@ struct RowStreamer {
       for (int v = 0; v < N; v++) open += hc[v] != N - 1;
       open_rows = open;
     }
+    // (one cudaMemcpyAsync per run of newly complete rows; the runtime's
+    // batched-copy entry point is closed on the target pool)
+    bdst.clear();
+    bsrc.clear();
+    bsz.clear();
     int u = 0;
     while (u < N) {
       if (sent[u] || (!all && hc[u] != N - 1)) { u++; continue; }
       int e = u;
       while (e < N && !sent[e] && (all || hc[e] == N - 1)) sent[e++] = 1;
-      CUDA_TRY(cudaMemcpyAsync(host + (size_t)u * N, s->D + (size_t)u * N, (size_t)(e - u) * N * 4,
-                               cudaMemcpyDeviceToHost, c->st3));
+      bdst.push_back(host + (size_t)u * N);
+      bsrc.push_back(s->D + (size_t)u * N);
+      bsz.push_back((size_t)(e - u) * N * 4);
       rows_sent += e - u;
       u = e;
     }
+    if (bdst.empty() || getenv("GP_E2E_NOCOPY")) return GP_OK;  // (timing probe: no row copies, results not delivered)
+    const auto t0 = std::chrono::steady_clock::now();
+    for (size_t i = 0; i < bdst.size(); i++) {
+      // Shallow copy queue: a fence event every FENCE copies, at most NFENCE
+      // fences outstanding.  (cudaMemcpyAsync into a full queue blocks inside
+      // the runtime, and with it the launches of the thread that drives the run.)
+      if (nfence_copies == FENCE) {
+        nfence_copies = 0;
+        cudaEvent_t& ev = fence[fence_head % NFENCE];
+        if (fence_head >= NFENCE) CUDA_TRY(cudaEventSynchronize(ev));
+        if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(ev, c->st3));
+        fence_head++;
+      }
+      nfence_copies++;
+      CUDA_TRY(cudaMemcpyAsync(bdst[i], bsrc[i], bsz[i], cudaMemcpyDeviceToHost, c->st3));
+    }
+    issue_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    issue_calls += (long long)bdst.size();
     return GP_OK;
   }
+  std::vector<void*> bdst, bsrc;
+  std::vector<size_t> bsz;
+  static constexpr int FENCE = 64, NFENCE = 4;
+  cudaEvent_t fence[NFENCE] = {nullptr, nullptr, nullptr, nullptr};
+  int nfence_copies = 0;
+  unsigned fence_head = 0;
+  double issue_ms = 0;       // host time spent issuing row copies
+  long long issue_calls = 0;
 };
 
 static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, int spec_k,
@@ -880,9 +927,12 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   EventPool evp;  // every event of the run, destroyed on all return paths
   unsigned long long* d_verify = nullptr;  // GP_VERIFY disagreement counter
   RowStreamer rs{c, s, D_host, {}, 0};
+  std::pair<uint2*, unsigned> patch_after_cut{nullptr, 0u};  // patch log and its position at the early send
+  unsigned h_ctl_final_patch_n = 0;
   if (D_host) {
     rs.sent.assign(N, 0);
     if (!c->st3) CUDA_TRY(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
+
     if (!c->h_cnt) CUDA_TRY(cudaHostAlloc(&c->h_cnt, (size_t)N * 4, cudaHostAllocDefault));
   }
   if (s->n != N) return fail(GP_EINVAL, "store size does not match the image");
@@ -1178,6 +1228,9 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       return GP_OK;
     };
     const bool pipelined = !debug && !(getenv("GP_PIPELINE") && !atoi(getenv("GP_PIPELINE")));
+    bool cut_done = false;           // gp_run_to_host: open rows sent early, later fills patched from the log
+    unsigned cut_n = 0;              // log position at the early send
+    unsigned long long cut_pairs = 0;
     if (pipelined) {
       // Device-gated pipeline: the host enqueues rounds of [commit, top-K,
       // propagation batch, list switch] on one stream; each kernel checks the
@@ -1211,6 +1264,11 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
         CUDA_TRY(cudaMemsetAsync(d_lb, 0, sizeof(LbCtl), st));
         ca.lb = d_lb;
         ca.lb_hits = d_hits;
+        if (D_host && !(getenv("GP_E2E_CUT") && atoll(getenv("GP_E2E_CUT")) < 0)) {
+          uint2* d_patch = nullptr;  // every list-mode fill is logged: at most one per list entry
+          CUDA_TRY(ws_get(c, WS_PATCH, &d_patch, (size_t)c->list_cap));
+          ca.patch = d_patch;
+        }
         ca.lb_debug = getenv("GP_LB_DEBUG") && atoi(getenv("GP_LB_DEBUG"));
         ca.lb_rcap = 1u << 30;  // GP_LB_RCAP (tests): records above it take the overflow path
         if (const char* e = getenv("GP_LB_RCAP")) ca.lb_rcap = (unsigned)std::max(0, atoi(e));
@@ -1255,43 +1313,128 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       if (int r = prop_batch(0)) return r;
       hmark("first batch enqueued");
       if (D_host) {
-        // Host rows: rounds with one round of lookahead.  Each round ends with
-        // copies of the counts and the control block into pinned buffers
-        // (alternating); while round r runs, the host reads round r-1's
-        // status and queues the D rows it completed on the copy stream, so
-        // the GPU never waits for the host (rows left after the last commit:
-        // ~400, 4 ms of D2H, against ~40 ms with the 6-round host checks).
+        // Host rows: rounds with LA rounds of lookahead.  Each round ends with
+        // a snapshot of the counts and the control block in pinned buffers
+        // (rotating); while rounds r-LA+1 .. r run or wait in the stream, the
+        // host reads round r-LA's status and queues the D rows it completed on
+        // the copy stream.  With one round of lookahead the GPU ran dry
+        // whenever the host needed longer for a round's row copies (~500
+        // cudaMemcpyAsync calls) than the GPU for the next round: 114 ms of
+        // stream gaps per 256x256 image; with two it never waits (rows left
+        // after the last commit: a few hundred, a few ms of D2H).
+        cut_pairs = 1500000;  // measured at 256x256 (e2e ms): 300 K 1437, 600 K 1423, 0.9-1.2 M 1413, 1.8 M 1404, 2.5 M 1430 (GP_E2E_CUT: pairs left at the early send; negative: off)
+        if (const char* e = getenv("GP_E2E_CUT")) cut_pairs = (unsigned long long)std::max(0ll, atoll(e));
         int e2e_cap = 0;  // GP_E2E_CAP: cap commit launches once half the rows are complete (0: off)
         if (const char* e = getenv("GP_E2E_CAP")) e2e_cap = atoi(e);
-        if (!c->h_cnt2) CUDA_TRY(cudaHostAlloc(&c->h_cnt2, (size_t)2 * N * 4, cudaHostAllocDefault));
-        if (!c->h_ctl2) CUDA_TRY(cudaHostAlloc(&c->h_ctl2, 2 * sizeof(Ctl), cudaHostAllocDefault));
-        cudaEvent_t rev[2];
-        CUDA_TRY(evp.make(&rev[0], cudaEventDisableTiming));
-        CUDA_TRY(evp.make(&rev[1], cudaEventDisableTiming));
+        // The host paces itself by the GPU, never by PCIe: it keeps KA rounds
+        // queued ahead of the run's stream (events of that stream), reads a
+        // round's snapshot whenever its copy has arrived (the copy queues
+        // behind the row copies -- up to ~100 ms late in the list phase, and
+        // waiting for it starved the GPU), and learns the end of the run from
+        // a flag the commit kernel writes into mapped host memory.
+        constexpr int NB = 8;  // snapshot buffers / round events (rotating; snapshots are monotone)
+        int KA = 3;
+        if (const char* e = getenv("GP_E2E_LOOKAHEAD")) KA = std::min(NB - 2, std::max(1, atoi(e)));
+        if (!c->h_cnt2) CUDA_TRY(cudaHostAlloc(&c->h_cnt2, (size_t)NB * N * 4, cudaHostAllocDefault));
+        if (!c->h_ctl2) CUDA_TRY(cudaHostAlloc(&c->h_ctl2, NB * sizeof(Ctl), cudaHostAllocDefault));
+        if (!c->h_done) CUDA_TRY(cudaHostAlloc(&c->h_done, sizeof(int), cudaHostAllocMapped));
+        if (!c->d_stage_cnt) CUDA_TRY(dalloc(&c->d_stage_cnt, (size_t)NB * N));
+        if (!c->d_stage_ctl) CUDA_TRY(dalloc(&c->d_stage_ctl, NB));
+        if (!c->st4) CUDA_TRY(cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking));
+        *(volatile int*)c->h_done = 0;
+        ca.h_done = c->h_done;
+        cudaEvent_t rev[NB], sev[NB];
+        for (int i = 0; i < NB; i++) {
+          CUDA_TRY(evp.make(&rev[i], cudaEventDisableTiming));
+          CUDA_TRY(evp.make(&sev[i], cudaEventDisableTiming));
+        }
         auto end_round = [&](int b) -> int {
-          CUDA_TRY(cudaMemcpyAsync(c->h_cnt2 + (size_t)b * N, s->cnt, (size_t)N * 4, cudaMemcpyDeviceToHost, st));
-          CUDA_TRY(cudaMemcpyAsync(c->h_ctl2 + b, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-          CUDA_TRY(cudaEventRecord(rev[b], st));
+          // stage on the run's stream (device only), copy out on the snapshot stream
+          CUDA_TRY(launch_stage(s->cnt, N, d_ctl, c->d_stage_cnt + (size_t)b * N, c->d_stage_ctl + b, st));
+          CUDA_TRY(cudaEventRecord(sev[b], st));
+          CUDA_TRY(cudaStreamWaitEvent(c->st4, sev[b], 0));
+          CUDA_TRY(cudaMemcpyAsync(c->h_cnt2 + (size_t)b * N, c->d_stage_cnt + (size_t)b * N, (size_t)N * 4,
+                                   cudaMemcpyDeviceToHost, c->st4));
+          CUDA_TRY(cudaMemcpyAsync(c->h_ctl2 + b, c->d_stage_ctl + b, sizeof(Ctl), cudaMemcpyDeviceToHost, c->st4));
+          CUDA_TRY(cudaEventRecord(rev[b], c->st4));
           return GP_OK;
         };
-        if (int r = round()) return r;
-        if (int r = end_round(0)) return r;
-        for (int rr = 1; rr < 8 * N + 16; rr++) {
-          if (int r = round()) return r;
-          if (int r = end_round(rr & 1)) return r;
-          const int b = (rr - 1) & 1;
-          CUDA_TRY(cudaEventSynchronize(rev[b]));  // round rr-1 done, round rr running
+        // one arrived snapshot: status, early send, row copies
+        auto process = [&](int round_idx) -> int {
+          const int b = round_idx % NB;
           const Ctl hc = c->h_ctl2[b];
-          if (hc.status == CTL_DONE) break;
-          if (hc.status == CTL_LIMIT && ca.max_steps > N) {
-            rc = fail(GP_EINTERNAL, "commit loop stopped unexpectedly");
-            break;
+          if (hc.status == CTL_LIMIT && ca.max_steps > N) return fail(GP_EINTERNAL, "commit loop stopped unexpectedly");
+          // Early send of the open rows.  Rows complete late: the last 13 000 of
+          // a 256x256 image in the last 100 ms, more than PCIe delivers in
+          // single-row copies.  Once few pairs are left (list mode), every row
+          // not sent yet goes out in large contiguous copies; the pairs filled
+          // from this snapshot on are in the device's patch log and are written
+          // into the host array after the run.
+          if (!cut_done && ca.patch && hc.mode == 1 && ca.total_pairs - hc.filled <= cut_pairs) {
+            cut_done = true;
+            cut_n = hc.patch_n;
+            if (int r = rs.enqueue(true, false)) return r;
+            if (htime) fprintf(stderr, "[gp host] early send at round %d (step %d): %llu pairs left, log position %u, at %.1f ms\n",
+                               round_idx, hc.step, ca.total_pairs - hc.filled, cut_n, hnow() - h0);
           }
+          if (cut_done) return GP_OK;
           if (int r = rs.enqueue(false, false, c->h_cnt2 + (size_t)b * N)) return r;
+          if (htime && round_idx % 8 == 0)
+            fprintf(stderr, "[gp host] round %d (step %d, mode %d): %lld rows queued at %.1f ms\n", round_idx, hc.step,
+                    hc.mode, (long long)rs.rows_sent, hnow() - h0);
           if (rs.open_rows >= 0 && rs.open_rows < N / 2 && e2e_cap > 0) ca.max_steps = e2e_cap;
+          return GP_OK;
+        };
+        // Row copies are issued by a second host thread: cudaMemcpyAsync blocks
+        // once the copy queue is full (the list phase completes rows faster
+        // than PCIe carries them), and blocked in it the launching thread left
+        // the GPU idle for ~100 ms of a 256x256 run.
+        std::atomic<int> nrounds{0}, stop{0}, wrc{0}, want_cap{0};
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        const int cap_req = e2e_cap;
+        e2e_cap = 0;  // (the worker requests the cap through want_cap)
+        std::thread worker([&] {
+          cudaSetDevice(dev);
+          for (int idx = 0;; idx++) {
+            while (idx >= nrounds.load(std::memory_order_acquire)) {
+              if (stop.load(std::memory_order_acquire) && idx >= nrounds.load(std::memory_order_acquire)) return;
+              std::this_thread::sleep_for(std::chrono::microseconds(50));
+            }
+            if (cudaEventSynchronize(rev[idx % NB]) != cudaSuccess) { wrc.store(GP_ECUDA); return; }
+            if (int r = process(idx)) { wrc.store(r); return; }
+            if (cap_req > 0 && rs.open_rows >= 0 && rs.open_rows < N / 2) want_cap.store(cap_req);
+          }
+        });
+        struct Joiner {  // every return path joins the worker
+          std::thread& t;
+          std::atomic<int>& stop;
+          ~Joiner() {
+            stop.store(1, std::memory_order_release);
+            if (t.joinable()) t.join();
+          }
+        } joiner{worker, stop};
+        for (int rr = 0; rr < 8 * N + 16 && !wrc.load(); rr++) {
+          if (*(volatile int*)c->h_done) break;  // the device completed the array
+          if (rr >= KA) CUDA_TRY(cudaEventSynchronize(sev[(rr - KA) % NB]));  // at most KA rounds ahead of the GPU
+          if (*(volatile int*)c->h_done) break;
+          if (int cp = want_cap.load()) ca.max_steps = cp;
+          if (int r = round()) return r;
+          if (int r = end_round(rr % NB)) return r;
+          nrounds.store(rr + 1, std::memory_order_release);
         }
+        hmark("device reported the end");
+        stop.store(1, std::memory_order_release);
+        worker.join();
+        if (wrc.load()) rc = fail(wrc.load(), "row streaming thread failed");
+        hmark("row thread joined");
+        hmark("host saw the end");
+        CUDA_TRY(cudaStreamSynchronize(c->st4));
+        hmark("snapshot stream drained");
         CUDA_TRY(cudaStreamSynchronize(st));
+        hmark("run stream drained");
         CUDA_TRY(cudaMemcpy(&h_ctl, d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+        hmark("control block read");
       }
       for (int guard = 0; !D_host && guard < 8 * N + 16; guard += chunk) {
         if (guard) rs.snapshot();  // quiescent point: the previous chunk is complete
@@ -1436,6 +1579,19 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     }
     for (auto& e : cev) S.ms_commit += ev_ms(e);
     for (auto& e : pev) S.ms_propagate += ev_ms(e);
+    if (htime && pipelined) {  // stream gaps between the timed kernels (GP_DEBUG_HOST)
+      double g1 = 0, g2 = 0, gmax = 0;
+      for (size_t i = 0; i + 1 < pev.size() && i < cev.size(); i++) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, pev[i].b, cev[i].a);      // batch i end -> commit launch i
+        cudaEventElapsedTime(&b, cev[i].b, pev[i + 1].a);  // commit launch i end -> batch i + 1
+        g1 += a;
+        g2 += b;
+        gmax = std::max(gmax, (double)std::max(a, b));
+      }
+      fprintf(stderr, "[gp host] stream gaps: batch->commit %.2f ms, commit->batch %.2f ms (max %.3f) over %zu rounds\n",
+              g1, g2, gmax, cev.size());
+    }
     P = h_ctl.step;
     S.propagations += h_ctl.total_props;
     if (cl_dbg.p) {
@@ -1466,6 +1622,10 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
                                                   " already-stored entries disagree with a committed tree");
     }
     S.visits = (int64_t)h_ctl.visits;
+    if (cut_done) {
+      patch_after_cut = {ca.patch, cut_n};
+      h_ctl_final_patch_n = h_ctl.patch_n;
+    }
   }
   if (D_host && !rc) {
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -1476,8 +1636,31 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     if (int r = rs.enqueue(true)) return r;
     CUDA_TRY(cudaStreamSynchronize(c->st3));
     hmark("final rows copied");
-    if (htime) fprintf(stderr, "[gp host] rows streamed during the run %lld, after %lld (open at last snapshot %d)\n",
-                       (long long)before, (long long)(rs.rows_sent - before), rs.open_rows);
+    if (patch_after_cut.first) {  // pairs filled after the early send
+      const unsigned n0 = patch_after_cut.second, n1 = h_ctl_final_patch_n;
+      if (n1 > n0) {
+        std::vector<uint2> pl((size_t)(n1 - n0));
+        CUDA_TRY(cudaMemcpy(pl.data(), patch_after_cut.first + n0, pl.size() * sizeof(uint2), cudaMemcpyDeviceToHost));
+        const int nt = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; t++)
+          th.emplace_back([&, t] {
+            for (size_t i = (size_t)t; i < pl.size(); i += (size_t)nt) {
+              const unsigned u = pl[i].x >> 16, w = pl[i].x & 0xFFFFu;
+              float v;
+              memcpy(&v, &pl[i].y, 4);
+              D_host[(size_t)u * N + w] = v;
+              D_host[(size_t)w * N + u] = v;
+            }
+          });
+        for (auto& x : th) x.join();
+      }
+      hmark("patches applied");
+      if (htime) fprintf(stderr, "[gp host] %u pairs patched into the host array\n", n1 - n0);
+    }
+    if (htime) fprintf(stderr, "[gp host] rows streamed during the run %lld, after %lld (open at last snapshot %d); "
+                       "%lld copy calls issued in %.1f ms of host time\n",
+                       (long long)before, (long long)(rs.rows_sent - before), rs.open_rows, rs.issue_calls, rs.issue_ms);
   }
   S.ms_total = ev_ms(tot);
   S.ms_setup = ev_ms(setup);

@@ -1007,6 +1007,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     a.ctl->list_dead = dead;
     a.ctl->list_cur = lcur;
     if (use_cand) a.ctl->cand_delta = cand_delta;
+    if (status == CTL_DONE && a.h_done) {  // gp_run_to_host: tell the host without a copy
+      *(volatile int*)a.h_done = 1;
+      __threadfence_system();
+    }
   }
 }
 
@@ -1516,6 +1520,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit_lb(CommitArgs a) {
         if (!rd) atomicAdd(&a.cnt[des], 1);
         list[i] = LIST_DEAD;
         atomicAdd(&newc[f], 1u);
+        if (a.patch)  // host rows sent before this pair was filled take it from the log
+          a.patch[atomicAdd(&a.ctl->patch_n, 1u)] = make_uint2(((unsigned)anc << 16) | (unsigned)des, __float_as_uint(duv));
       }
     }
     __syncthreads();
@@ -1589,6 +1595,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit_lb(CommitArgs a) {
     a.ctl->list_dead = s_dead;
     a.ctl->list_cur = lcur;
     a.ctl->cand_delta = cand_delta;
+    if (status == CTL_DONE && a.h_done) {  // gp_run_to_host: tell the host without a copy
+      *(volatile int*)a.h_done = 1;
+      __threadfence_system();
+    }
   }
 }
 
@@ -2027,6 +2037,24 @@ cudaError_t launch_merge_sym(float* D, int N, cudaStream_t st) {
   const long long T = (N + 31) / 32;
   const long long pairs = T * (T + 1) / 2;
   k_merge_sym<<<(unsigned)pairs, 256, 0, st>>>(D, N, (int)T);
+  return cudaGetLastError();
+}
+
+// Round status for the host (gp_run_to_host): counts and control block staged
+// in device memory by a kernel on the run's stream; a second stream copies the
+// stage to pinned host memory.  Anything the run's own stream sends to the
+// host -- a D2H copy or stores to mapped memory, 256 KB or 2 KB -- waits
+// ~0.9 ms behind the row copies in flight, and the next kernel with it: 114 ms
+// of stalls per 256x256 image.
+__global__ void k_stage(const int* cnt, int N, const Ctl* ctl, int* s_cnt, Ctl* s_ctl) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) s_cnt[v] = __ldcg(&cnt[v]);
+  if (blockIdx.x == 0 && threadIdx.x < (int)(sizeof(Ctl) / 4))
+    reinterpret_cast<int*>(s_ctl)[threadIdx.x] = __ldcg(reinterpret_cast<const int*>(ctl) + threadIdx.x);
+}
+
+cudaError_t launch_stage(const int* cnt, int N, const Ctl* ctl, int* s_cnt, Ctl* s_ctl, cudaStream_t st) {
+  static_assert(sizeof(Ctl) % 4 == 0 && sizeof(Ctl) / 4 <= 256, "control block copied by one CTA");
+  k_stage<<<std::min(64, (N + 255) / 256), 256, 0, st>>>(cnt, N, ctl, s_cnt, s_ctl);
   return cudaGetLastError();
 }
 

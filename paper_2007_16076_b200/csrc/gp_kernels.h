@@ -97,6 +97,7 @@ struct Ctl {
   int build;                       // list build pending (set by k_switch_prep)
   unsigned cand_delta;             // candidate-set width in counts (k_commit, adaptive)
   unsigned cand_cnt[3];            // candidate collection counters (k_commit: step parity; k_commit_lb: rotating)
+  unsigned patch_n;                // pairs logged in CommitArgs::patch (gp_run_to_host, list mode)
 };
 enum { CTL_RUNNING = 0, CTL_DONE = 1, CTL_MISS = 2, CTL_LIMIT = 3, CTL_SWITCH = 4 };
 
@@ -143,6 +144,9 @@ struct CommitArgs {
   unsigned long long* dbgo; // optional per-step open-pixel counts (debug dump)
   GridBarrier* bar;
   uint32_t* plist[2];      // unfilled pairs (u << 16 | w, u < w), list mode
+  uint2* patch;            // gp_run_to_host: log of the pairs filled in list mode (anc << 16 | des, value bits);
+                           // nullptr: off.  Rows sent to the host early are patched from it.
+  int* h_done;             // mapped host flag set when the array is complete (gp_run_to_host; nullptr: off)
   int one_sided;           // tree fills store D[anc][des] only (launch_merge_sym completes D after the run)
   LbCtl* lb;               // batched list-mode commits (nullptr: one commit per step)
   unsigned long long* lb_hits;  // [list capacity] entry index << 16 | J
@@ -179,6 +183,7 @@ cudaError_t launch_switch(const CommitArgs& a, uint32_t* list0, cudaStream_t st)
 // ---------------- store helpers ----------------
 cudaError_t launch_store_init(const MarkLayout& L, uint32_t* mark, float* D, cudaStream_t st);
 cudaError_t launch_merge_sym(float* D, int N, cudaStream_t st);
+cudaError_t launch_stage(const int* cnt, int N, const Ctl* ctl, int* s_cnt, Ctl* s_ctl, cudaStream_t st);
 // filling-rate ranking on the device (setup.cu): ext / rank from dist_from_c
 size_t ext_rank_temp_bytes(int N);
 cudaError_t launch_ext_rank(const float* dfc, int N, unsigned long long* keys2, void* temp,

@@ -32,5 +32,5 @@ for rep in range(4):
                                 ctypes.c_void_p(Dh.data_ptr())))
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    print(f"rep{rep} load {1e3*(t1-t0):.2f} ms  run_to_host wall {1e3*(t2-t1):.1f} ms  device {s.ms_total:.1f} ms"
+    print(f"rep{rep} commit {s.ms_commit:.1f} prop {s.ms_propagate:.1f} load {1e3*(t1-t0):.2f} ms  run_to_host wall {1e3*(t2-t1):.1f} ms  device {s.ms_total:.1f} ms"
           f"  -> host/copy overhead {1e3*(t2-t1)-s.ms_total:.1f} ms", flush=True)

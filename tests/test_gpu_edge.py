@@ -157,15 +157,22 @@ def test_metric_properties_of_completed_array(gp):
     assert int((D[x, z] > D[x, y] + D[y, z]).sum()) == 0
 
 
-@pytest.mark.parametrize("shape,kind,cap", [((40, 37), 1, 0), ((64, 64), 1, 0), ((23, 30), 0, 0),
-                                            ((64, 64), 1, 3)])
-def test_run_to_host_streams_the_same_array(gp, shape, kind, cap, monkeypatch):
+@pytest.mark.parametrize("shape,kind,cap,cut", [((40, 37), 1, 0, None), ((64, 64), 1, 0, None), ((23, 30), 0, 0, None),
+                                                ((64, 64), 1, 3, None), ((64, 64), 1, 0, 10 ** 9),
+                                                ((64, 64), 1, 0, 20000), ((96, 100), 1, 0, 2000000),
+                                                ((96, 100), 2, 0, 100000), ((96, 100), 1, 0, -1)])
+def test_run_to_host_streams_the_same_array(gp, shape, kind, cap, cut, monkeypatch):
     """gp_run_to_host (rows streamed during the run) == gp_run + gp_store_read;
-    cap > 0: GP_E2E_CAP (short commit launches once half the rows are done)."""
+    cap > 0: GP_E2E_CAP (short commit launches once half the rows are done);
+    cut: GP_E2E_CUT with the batched list kernel (open rows sent early once that many
+    pairs are left, later fills patched into the host array from the device's log)."""
     import ctypes
 
     if cap:
         monkeypatch.setenv("GP_E2E_CAP", str(cap))
+    if cut is not None:
+        monkeypatch.setenv("GP_E2E_CUT", str(cut))
+        monkeypatch.setenv("GP_LIST_BATCH", "1")
 
     import torch
 
