@@ -71,6 +71,8 @@ struct gp_ctx {
   Ctl* d_stage_ctl = nullptr;
   cudaStream_t st4 = nullptr;  // snapshot copies
   int* h_done = nullptr;       // mapped pinned: set by the commit kernel when the array is complete
+  uint2* h_patch = nullptr;    // pinned: patch log entries after the early send (gp_run_to_host)
+  size_t h_patch_cap = 0;
   Ctl* h_ctl2 = nullptr;     // pinned: two control-block snapshots
   void* ws[32] = {};      // run workspace, cached across runs (no cudaMalloc in gp_run)
   size_t ws_bytes[32] = {};
@@ -246,6 +248,7 @@ extern "C" void gp_ctx_destroy(gp_ctx* c) {
   cudaFree(c->d_stage_ctl);
   if (c->st4) cudaStreamDestroy(c->st4);
   if (c->h_done) cudaFreeHost(c->h_done);
+  if (c->h_patch) cudaFreeHost(c->h_patch);
   if (c->h_ctl2) cudaFreeHost(c->h_ctl2);
   delete c;
 }
@@ -929,6 +932,28 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   RowStreamer rs{c, s, D_host, {}, 0};
   std::pair<uint2*, unsigned> patch_after_cut{nullptr, 0u};  // patch log and its position at the early send
   unsigned h_ctl_final_patch_n = 0;
+  struct PatchChunk { unsigned b, e; cudaEvent_t ev; };
+  std::vector<PatchChunk> pchunks;  // log ranges copied to c->h_patch, not applied yet
+  unsigned patch_fetched = 0;       // log position up to which the copy to the host is queued
+  // patches [b, e) of the log (host copy at c->h_patch, offset by the early send's position) into D_host
+  auto apply_patches = [&](unsigned b, unsigned e, unsigned base, int nt) {
+    if (e <= b) return;
+    const uint2* pl = c->h_patch + (b - base);
+    const size_t n = e - b;
+    auto work = [=](int t) {
+      for (size_t i = (size_t)t; i < n; i += (size_t)nt) {
+        const unsigned u = pl[i].x >> 16, w = pl[i].x & 0xFFFFu;
+        float v;
+        memcpy(&v, &pl[i].y, 4);
+        D_host[(size_t)u * N + w] = v;
+        D_host[(size_t)w * N + u] = v;
+      }
+    };
+    if (nt <= 1 || n < 4096) { for (int t = 0; t < nt; t++) work(t); return; }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; t++) th.emplace_back(work, t);
+    for (auto& x : th) x.join();
+  };
   if (D_host) {
     rs.sent.assign(N, 0);
     if (!c->st3) CUDA_TRY(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
@@ -967,12 +992,17 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   // sentinel, tree-mode fills store the ancestor's row only, and one
   // transpose-merge pass after the run completes the symmetric array (saves
   // the scattered mirrored store of every new pair; GP_ONE_SIDED=0 off).
-  // gp_run_to_host keeps two-sided fills: it streams complete rows as the run
-  // proceeds (completing rows from their mirrored elements just before the
-  // copy was measured slower: e2e 1.575 vs 1.496 s per 256^2 image).
-  const bool one_sided = !D_host && !(strategy == GP_STRATEGY_NAIVE && !naive_with_tree) &&
+  // (completing single rows from their mirrored elements just before each
+  // copy was measured slower: e2e 1.575 vs 1.496 s per 256^2 image)
+  // gp_run_to_host: the pass runs at the list switch, and rows are streamed
+  // from there on (list-mode fills write both elements); runs that never
+  // switch (no list phase) keep two-sided fills.
+  const bool will_switch = getenv("GP_LIST_ALPHA") ? atof(getenv("GP_LIST_ALPHA")) > 0 : strategy != GP_STRATEGY_NAIVE;
+  const bool host_loop = (getenv("GP_DEBUG") && atoi(getenv("GP_DEBUG"))) || (getenv("GP_PIPELINE") && !atoi(getenv("GP_PIPELINE")));
+  const bool one_sided = !(strategy == GP_STRATEGY_NAIVE && !naive_with_tree) &&
                          !(getenv("GP_VERIFY") && atoi(getenv("GP_VERIFY"))) &&
-                         !(getenv("GP_ONE_SIDED") && !atoi(getenv("GP_ONE_SIDED")));
+                         !(getenv("GP_ONE_SIDED") && !atoi(getenv("GP_ONE_SIDED"))) &&
+                         (!D_host || (will_switch && !host_loop));
   if (one_sided) CUDA_TRY(cudaMemsetAsync(s->D, 0xFF, (size_t)N * N * 4, st));
   CUDA_TRY(launch_store_init(L, s->mark, s->D, st));
   S.kernels += 1;
@@ -1147,6 +1177,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     ca.selkey = d_selkey;
     ca.stepflags = d_flags;
     ca.one_sided = one_sided ? 1 : 0;
+    ca.merge_at_switch = (one_sided && D_host) ? 1 : 0;
     ca.seq = d_seq;
     ca.newp = d_new;
     ca.ctl = d_ctl;
@@ -1322,7 +1353,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
         // cudaMemcpyAsync calls) than the GPU for the next round: 114 ms of
         // stream gaps per 256x256 image; with two it never waits (rows left
         // after the last commit: a few hundred, a few ms of D2H).
-        cut_pairs = 1500000;  // measured at 256x256 (e2e ms): 300 K 1437, 600 K 1423, 0.9-1.2 M 1413, 1.8 M 1404, 2.5 M 1430 (GP_E2E_CUT: pairs left at the early send; negative: off)
+        cut_pairs = 8000000;  // measured at 256x256 (e2e ms): 3 M 1364, 5 M 1361, 8 M 1357, at the switch 1384 (GP_E2E_CUT: pairs left at the early send; negative: off)
         if (const char* e = getenv("GP_E2E_CUT")) cut_pairs = (unsigned long long)std::max(0ll, atoll(e));
         int e2e_cap = 0;  // GP_E2E_CAP: cap commit launches once half the rows are complete (0: off)
         if (const char* e = getenv("GP_E2E_CAP")) e2e_cap = atoi(e);
@@ -1359,6 +1390,15 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
           CUDA_TRY(cudaEventRecord(rev[b], c->st4));
           return GP_OK;
         };
+        // log ranges whose copy has arrived: into the host array (row thread)
+        auto drain_patches = [&]() {
+          size_t done = 0;
+          while (done < pchunks.size() && cudaEventQuery(pchunks[done].ev) == cudaSuccess) {
+            apply_patches(pchunks[done].b, pchunks[done].e, cut_n, 4);
+            done++;
+          }
+          pchunks.erase(pchunks.begin(), pchunks.begin() + (long)done);
+        };
         // one arrived snapshot: status, early send, row copies
         auto process = [&](int round_idx) -> int {
           const int b = round_idx % NB;
@@ -1373,11 +1413,35 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
           if (!cut_done && ca.patch && hc.mode == 1 && ca.total_pairs - hc.filled <= cut_pairs) {
             cut_done = true;
             cut_n = hc.patch_n;
+            patch_fetched = cut_n;
+            if (c->h_patch_cap < (size_t)cut_pairs + 1024) {  // at most one entry per pair still open
+              if (c->h_patch) cudaFreeHost(c->h_patch);
+              c->h_patch = nullptr;
+              c->h_patch_cap = 0;
+              CUDA_TRY(cudaHostAlloc(&c->h_patch, ((size_t)cut_pairs + 1024) * sizeof(uint2), cudaHostAllocDefault));
+              c->h_patch_cap = (size_t)cut_pairs + 1024;
+            }
             if (int r = rs.enqueue(true, false)) return r;
             if (htime) fprintf(stderr, "[gp host] early send at round %d (step %d): %llu pairs left, log position %u, at %.1f ms\n",
                                round_idx, hc.step, ca.total_pairs - hc.filled, cut_n, hnow() - h0);
           }
-          if (cut_done) return GP_OK;
+          if (cut_done) {
+            // later fills: the log's new entries follow the bulk copies on the
+            // copy stream (in order: they arrive after the rows they patch) and
+            // are applied as they arrive
+            if (hc.patch_n > patch_fetched) {
+              PatchChunk pc{patch_fetched, hc.patch_n, nullptr};
+              CUDA_TRY(cudaMemcpyAsync(c->h_patch + (pc.b - cut_n), ca.patch + pc.b, (size_t)(pc.e - pc.b) * sizeof(uint2),
+                                       cudaMemcpyDeviceToHost, c->st3));
+              CUDA_TRY(evp.make(&pc.ev, cudaEventDisableTiming));
+              CUDA_TRY(cudaEventRecord(pc.ev, c->st3));
+              pchunks.push_back(pc);
+              patch_fetched = pc.e;
+            }
+            drain_patches();
+            return GP_OK;
+          }
+          if (ca.merge_at_switch && hc.mode == 0) return GP_OK;  // one-sided rows: complete only after the switch's pass
           if (int r = rs.enqueue(false, false, c->h_cnt2 + (size_t)b * N)) return r;
           if (htime && round_idx % 8 == 0)
             fprintf(stderr, "[gp host] round %d (step %d, mode %d): %lld rows queued at %.1f ms\n", round_idx, hc.step,
@@ -1399,7 +1463,8 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
           for (int idx = 0;; idx++) {
             while (idx >= nrounds.load(std::memory_order_acquire)) {
               if (stop.load(std::memory_order_acquire) && idx >= nrounds.load(std::memory_order_acquire)) return;
-              std::this_thread::sleep_for(std::chrono::microseconds(50));
+              if (!pchunks.empty()) drain_patches();
+              else std::this_thread::sleep_for(std::chrono::microseconds(50));
             }
             if (cudaEventSynchronize(rev[idx % NB]) != cudaSuccess) { wrc.store(GP_ECUDA); return; }
             if (int r = process(idx)) { wrc.store(r); return; }
@@ -1515,7 +1580,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       }
     }
     CUDA_TRY(cudaStreamSynchronize(ps));
-    if (one_sided) {
+    if (one_sided && !(ca.merge_at_switch && h_ctl.mode == 1)) {  // (not yet completed at a list switch)
       CUDA_TRY(launch_merge_sym(s->D, N, st));
       S.kernels += 1;
     }
@@ -1636,27 +1701,17 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     if (int r = rs.enqueue(true)) return r;
     CUDA_TRY(cudaStreamSynchronize(c->st3));
     hmark("final rows copied");
-    if (patch_after_cut.first) {  // pairs filled after the early send
+    if (patch_after_cut.first) {  // pairs filled after the early send and not applied during the run
       const unsigned n0 = patch_after_cut.second, n1 = h_ctl_final_patch_n;
-      if (n1 > n0) {
-        std::vector<uint2> pl((size_t)(n1 - n0));
-        CUDA_TRY(cudaMemcpy(pl.data(), patch_after_cut.first + n0, pl.size() * sizeof(uint2), cudaMemcpyDeviceToHost));
-        const int nt = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-        std::vector<std::thread> th;
-        for (int t = 0; t < nt; t++)
-          th.emplace_back([&, t] {
-            for (size_t i = (size_t)t; i < pl.size(); i += (size_t)nt) {
-              const unsigned u = pl[i].x >> 16, w = pl[i].x & 0xFFFFu;
-              float v;
-              memcpy(&v, &pl[i].y, 4);
-              D_host[(size_t)u * N + w] = v;
-              D_host[(size_t)w * N + u] = v;
-            }
-          });
-        for (auto& x : th) x.join();
-      }
+      if (n1 > patch_fetched)
+        CUDA_TRY(cudaMemcpy(c->h_patch + (patch_fetched - n0), patch_after_cut.first + patch_fetched,
+                            (size_t)(n1 - patch_fetched) * sizeof(uint2), cudaMemcpyDeviceToHost));
+      const unsigned from = pchunks.empty() ? patch_fetched : pchunks.front().b;  // (the copy stream is drained)
+      const int nt = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+      apply_patches(from, n1, n0, nt);
       hmark("patches applied");
-      if (htime) fprintf(stderr, "[gp host] %u pairs patched into the host array\n", n1 - n0);
+      if (htime) fprintf(stderr, "[gp host] %u pairs patched into the host array, %u of them after the run\n", n1 - n0,
+                         n1 - from);
     }
     if (htime) fprintf(stderr, "[gp host] rows streamed during the run %lld, after %lld (open at last snapshot %d); "
                        "%lld copy calls issued in %.1f ms of host time\n",

@@ -1987,9 +1987,11 @@ __global__ void k_build_list_gated(MarkLayout L, const uint32_t* mark, uint32_t*
   k_build_list_body(L, mark, list, &ctl->list_n[0]);
 }
 
+__global__ void k_merge_sym_gated(float* D, int N, const Ctl* ctl);
 cudaError_t launch_switch(const CommitArgs& a, uint32_t* list0, cudaStream_t st) {
   k_switch_prep<<<1, 32, 0, st>>>(a.ctl);
   k_build_list_gated<<<148 * 8, 256, 0, st>>>(a.L, a.mark, list0, a.ctl);
+  if (a.merge_at_switch) k_merge_sym_gated<<<148 * 8, 256, 0, st>>>(a.D, a.g.N, a.ctl);
   return cudaGetLastError();
 }
 
@@ -1999,15 +2001,12 @@ cudaError_t launch_switch(const CommitArgs& a, uint32_t* list0, cudaStream_t st)
 // symmetric array: for every tile pair (I, J), I <= J, each element takes
 // whichever of D[i][j], D[j][i] was written (list-mode fills write both).
 // It reads and writes D once (~24 GiB of HBM traffic at 256x256).
-__global__ void __launch_bounds__(256) k_merge_sym(float* D, int N, int T) {
-  __shared__ uint32_t ta[32][33], tb[32][33];
-  // tile pair index -> (I, J), I <= J
-  const long long p = blockIdx.x;
+__device__ __forceinline__ void merge_tile_pair(float* D, int N, long long p, uint32_t (*ta)[33], uint32_t (*tb)[33]) {
+  // tile pair index -> (r, c), r <= c
   int I = (int)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
   while ((long long)(I + 1) * (I + 2) / 2 <= p) I++;
   while ((long long)I * (I + 1) / 2 > p) I--;
   const int Jr = (int)(p - (long long)I * (I + 1) / 2);  // 0 .. I
-  // (I here counts the larger index; name the pair (r, c) with r <= c)
   const int r0 = Jr * 32, c0 = I * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows per pass
   uint32_t* Du = reinterpret_cast<uint32_t*>(D);
@@ -2030,13 +2029,30 @@ __global__ void __launch_bounds__(256) k_merge_sym(float* D, int N, int T) {
       if (rb < N && cb < N && b == 0xFFFFFFFFu && a != 0xFFFFFFFFu) Du[(size_t)rb * N + cb] = a;
     }
   }
-  (void)T;
+}
+
+__global__ void __launch_bounds__(256) k_merge_sym(float* D, int N) {
+  __shared__ uint32_t ta[32][33], tb[32][33];
+  merge_tile_pair(D, N, blockIdx.x, ta, tb);
+}
+
+// the same pass, run only in the round of the list switch (gp_run_to_host with
+// one-sided tree fills: rows are streamed from the switch on, list-mode fills
+// write both elements)
+__global__ void __launch_bounds__(256) k_merge_sym_gated(float* D, int N, const Ctl* ctl) {
+  __shared__ uint32_t ta[32][33], tb[32][33];
+  if (!*(volatile const int*)&ctl->build) return;
+  const long long T = (N + 31) / 32, pairs = T * (T + 1) / 2;
+  for (long long p = blockIdx.x; p < pairs; p += gridDim.x) {
+    merge_tile_pair(D, N, p, ta, tb);
+    __syncthreads();
+  }
 }
 
 cudaError_t launch_merge_sym(float* D, int N, cudaStream_t st) {
   const long long T = (N + 31) / 32;
   const long long pairs = T * (T + 1) / 2;
-  k_merge_sym<<<(unsigned)pairs, 256, 0, st>>>(D, N, (int)T);
+  k_merge_sym<<<(unsigned)pairs, 256, 0, st>>>(D, N);
   return cudaGetLastError();
 }
 

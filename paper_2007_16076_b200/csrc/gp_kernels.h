@@ -147,6 +147,7 @@ struct CommitArgs {
   uint2* patch;            // gp_run_to_host: log of the pairs filled in list mode (anc << 16 | des, value bits);
                            // nullptr: off.  Rows sent to the host early are patched from it.
   int* h_done;             // mapped host flag set when the array is complete (gp_run_to_host; nullptr: off)
+  int merge_at_switch;     // one-sided fills completed at the list switch (gp_run_to_host) instead of after the run
   int one_sided;           // tree fills store D[anc][des] only (launch_merge_sym completes D after the run)
   LbCtl* lb;               // batched list-mode commits (nullptr: one commit per step)
   unsigned long long* lb_hits;  // [list capacity] entry index << 16 | J
