@@ -16,10 +16,10 @@ see DESIGN.md), value = N * A * K / max-over-ranks(device time of K steps).
   gp_ctx_load (validation + H2D of the image from pinned memory) +
   gp_run_to_host (the run, with D streamed into pinned host memory as its
   rows complete: D2H 4*N^2 bytes); wall clock around the synchronous calls.
-* roofline: dominant kernel = the commit loop (k_commit).  Algorithmic bytes
+* roofline: dominant kernel = the commit loop (k_commit + k_commit_lb).  Algorithmic bytes
   per image B_alg = 4N^2 + N^2/8 + C/4 + 10*N*P with C the
   ancestor/descendant pairs of the committed trees (measured on device),
-  divided by the summed k_commit event time.
+  divided by the summed commit-launch event time.
 * cpu_baseline (rank 0, N=1): the oracle port (oracle/, C; the reference
   rejects fp32 images) on 1 host core -- the reference is single-threaded --
   over two prefixes of the run, whole image extrapolated from the marginal
@@ -117,10 +117,11 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def _traffic(config: int, kernel: str):
-    """DRAM bytes (read + write) of `kernel` summed over one image's launches,
-    from the newest committed ncu capture profiles/*_cfg<config>_traffic.json
-    (scripts/ncu_traffic.py); None when there is none."""
+def _traffic(config: int, kernels):
+    """DRAM bytes (read + write) of `kernels` (names of the traffic file)
+    summed over one image's launches, from the newest committed ncu capture
+    profiles/*_cfg<config>_traffic.json (scripts/ncu_traffic.py); None when
+    there is none."""
     import glob
 
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_cfg{config}_traffic.json")))
@@ -128,8 +129,14 @@ def _traffic(config: int, kernel: str):
         return None, None
     try:
         with open(files[-1]) as f:
-            k = json.load(f)["kernels"][kernel]
-        return k, os.path.relpath(files[-1], ROOT)
+            ks = json.load(f)["kernels"]
+        found = [ks[k] for k in kernels if k in ks]
+        if not found:
+            return None, None
+        tot = {"launches": sum(k["launches"] for k in found), "dram_bytes": sum(k["dram_bytes"] for k in found),
+               "ms": sum(k["ms"] for k in found)}
+        tot["dram_bytes_per_launch"] = tot["dram_bytes"] / max(tot["launches"], 1)
+        return tot, os.path.relpath(files[-1], ROOT)
     except Exception:
         return None, None
 
@@ -412,8 +419,11 @@ def main():
     if spec.strategy == "naive":
         b_alg = 4.0 * N * N + N * N / 8.0 + 10.0 * N * P
         achieved = b_alg / (prop_ms / 1e3) / 1e9
-    kname = "k_commit" if spec.strategy != "naive" else "k_propagate"
-    tk, tsrc = _traffic(args.config, kname)
+    # the commit loop: tree-mode k_commit, batched list-mode k_commit_lb, and the
+    # transpose-merge pass that completes the one-sided tree fills
+    knames = ["k_commit", "k_commit_lb", "k_merge_sym"] if spec.strategy != "naive" else ["k_propagate"]
+    kname = " + ".join(knames)
+    tk, tsrc = _traffic(args.config, knames)
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -430,6 +440,10 @@ def main():
                                        f"({tsrc}); achieved uses the same per-image scope") if tk else None,
                      "traffic_per_launch": tk["dram_bytes_per_launch"] if tk else None,
                      "traffic_over_algorithmic": tk["dram_bytes"] / b_alg if tk else None,
+                     # the store reset fills D with the one-sided fills' sentinel by a driver memset
+                     # (4N^2 bytes written once, not a kernel in the ncu list): counted here
+                     "traffic_over_algorithmic_with_store_reset": ((tk["dram_bytes"] + 4.0 * N * N) / b_alg
+                                                                    if tk and spec.strategy != "naive" else None),
                      "peak_kind": peak_kind, "kernel": kname,
                      "algorithmic_bytes_per_image": b_alg, "C_visits": C,
                      "kernel_ms_per_image": commit_ms if spec.strategy != "naive" else prop_ms},

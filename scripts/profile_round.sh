@@ -21,11 +21,11 @@ timeout 900 $NCU --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_
   --log-file $O/${TAG}_cfg${CFG}_traffic.csv python scripts/one_run.py $CFG > $O/${TAG}_ncu_traffic.log 2>&1
 echo "traffic exit $?"
 echo "== full captures"
-# mode-specific commit kernels (mangled names: ...ELi0E tree mode, ...ELi1E list mode)
+# tree-mode commit kernel (mangled name ...ELi0E) and the batched list-mode kernel k_commit_lb
 timeout 900 $NCU --set full --import-source on --kernel-name-base mangled -k regex:k_commitILi4ELi1024ELi1ELi0E --launch-skip 20 --launch-count 1 \
   -o $O/${TAG}_cfg${CFG}_k_commit_tree -f python scripts/one_run.py $CFG > $O/${TAG}_ncu_commit_tree.log 2>&1
 echo "commit tree exit $?"
-timeout 900 $NCU --set full --import-source on --kernel-name-base mangled -k regex:k_commitILi4ELi1024ELi1ELi1E --launch-skip 100 --launch-count 1 \
+timeout 900 $NCU --set full --import-source on -k regex:k_commit_lb --launch-skip 100 --launch-count 1 \
   -o $O/${TAG}_cfg${CFG}_k_commit_list -f python scripts/one_run.py $CFG > $O/${TAG}_ncu_commit_list.log 2>&1
 echo "commit list exit $?"
 GP_PIPELINE=0 timeout 900 $NCU --set full --import-source on -k regex:k_propagate --launch-skip 40 --launch-count 1 \

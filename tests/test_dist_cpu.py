@@ -61,11 +61,14 @@ def test_committed_traffic_evidence_feeds_roofline():
     headline config; the commit kernels' bytes must be present and consistent."""
     import bench
 
-    k, src = bench._traffic(5, "k_commit")
+    k, src = bench._traffic(5, ["k_commit", "k_commit_lb", "k_merge_sym"])
     assert src is not None and src.startswith("profiles/")
     assert k["launches"] > 0 and k["dram_bytes"] > 0
     assert abs(k["dram_bytes_per_launch"] * k["launches"] - k["dram_bytes"]) < 1e-6 * k["dram_bytes"]
-    assert bench._traffic(999, "k_commit") == (None, None)
+    one, _ = bench._traffic(5, ["k_commit"])
+    assert 0 < one["dram_bytes"] <= k["dram_bytes"]
+    assert bench._traffic(999, ["k_commit"]) == (None, None)
+    assert bench._traffic(5, ["no_such_kernel"]) == (None, None)
 
 
 def test_both_arms_share_the_config_dict():
