@@ -257,7 +257,7 @@ extern "C" int gp_ctx_num_pixels(const gp_ctx* c) { return c ? c->g.N : 0; }
 
 enum { WS_SEQ, WS_NEW, WS_SRC, WS_SLOT_OF, WS_RANK, WS_EXT, WS_SELKEY, WS_FLAGS, WS_CTL, WS_DFC,
        WS_FREE, WS_CANDS, WS_SLOTS, WS_BORDER, WS_CEN, WS_FB, WS_TOPK, WS_EXTK, WS_EXTT, WS_CSET,
-       WS_VERIFY, WS_CS_SRC, WS_CS_DIST, WS_CS_DIR, WS_CS_PAR, WS_LB, WS_LBHITS, WS_LBTINB, WS_PATCH, WS_SBIG };
+       WS_VERIFY, WS_CS_SRC, WS_CS_DIST, WS_CS_DIR, WS_CS_PAR, WS_LB, WS_LBHITS, WS_LBTINB, WS_PATCH };
 
 template <typename T>
 static cudaError_t ws_get(gp_ctx* c, int id, T** p, size_t count) {
@@ -1178,17 +1178,6 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     ca.stepflags = d_flags;
     ca.one_sided = one_sided ? 1 : 0;
     ca.merge_at_switch = (one_sided && D_host) ? 1 : 0;
-    // row scans of big ancestors in the tree phase (commit.cu scan_row_part); GP_SCAN=0 off
-    if (!verify && getenv("GP_SCAN") && atoi(getenv("GP_SCAN")) != 0) {
-      unsigned* d_sbig = nullptr;
-      CUDA_TRY(ws_get(c, WS_SBIG, &d_sbig, N + 4));
-      CUDA_TRY(cudaMemsetAsync(d_sbig, 0xFF, (size_t)(N + 4) * 4, st));
-      ca.sbigv = d_sbig;
-      ca.scan_min = 2048;
-      ca.scan_mult4 = 8;
-      if (const char* e = getenv("GP_SCAN_MIN")) ca.scan_min = (unsigned)std::max(32, atoi(e));
-      if (const char* e = getenv("GP_SCAN_MULT4")) ca.scan_mult4 = (unsigned)std::max(0, atoi(e));
-    }
     ca.seq = d_seq;
     ca.newp = d_new;
     ca.ctl = d_ctl;

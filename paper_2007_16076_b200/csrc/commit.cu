@@ -196,109 +196,10 @@ __device__ __forceinline__ void verify_pair(const CommitArgs& a, float stored, f
 // the inner loop is load entry -> load mark word of row u -> test bit, U
 // iterations in flight.  The fill is instruction-issue bound, so the loop is
 // kept to a handful of instructions per tested pair.
-// Row scans of big ancestors (tree mode).  Late in the tree phase a trunk
-// ancestor u still owns thousands of 32-pair chunks although its row has few
-// unfilled columns left.  When the step's threshold sb is set, ancestors with
-// >= sb descendants emit no chunks; the unit that owns chunk 0 of such an
-// ancestor queues its preorder position instead, and after the chunk queue is
-// drained the CTA's warps scan row u of the mark bitmap word by word and test
-// only the unset columns against u's Euler interval (scan_row_part).  The
-// decision depends on the tree and the step-uniform sb alone, so every unit
-// of an ancestor decides alike.
-#ifndef GP_SQ_CAP
-#define GP_SQ_CAP 1024
-#endif
-#ifndef GP_SCAN_IT
-#define GP_SCAN_IT 4  // 32-word loads in flight per lane; one scan item = 32 * GP_SCAN_IT words
-#endif
-constexpr int SQ_CAP = GP_SQ_CAP;
-constexpr int SCAN_IT = GP_SCAN_IT;
-constexpr unsigned SCAN_W = 32u * SCAN_IT;
-struct ScanQ {
-  uint16_t q[SQ_CAP];
-  int n, head;
-};
-
-// one item of a row scan: words [blk * SCAN_W, +SCAN_W) of the row of the
-// ancestor at preorder position q (warp-collective; returns the new pairs on
-// lane 0)
-__device__ __forceinline__ unsigned scan_row_part(const CommitArgs& a, int slot, unsigned q,
-                                                  unsigned blk) {
-  const int N = a.g.N;
-  const int lane = threadIdx.x & 31;
-  const size_t off = (size_t)slot * N;
-  const MarkLayout L = a.L;
-  const uint32_t eu = __ldg(&a.ts.pre[off + q]);
-  const unsigned szu = __ldg(&a.ts.szp[off + q]);
-  const int u = (int)(eu & 0xFFFFu);
-  const uint32_t ucol = eu >> 16;
-  if (__ldcg(&a.cnt[u]) >= N - 1) return 0u;
-  const uint32_t* tinz = a.ts.tin + off;
-  const float* tdp = a.ts.tdp + off;
-  uint32_t* row = a.mark + (size_t)u * L.RW;
-  uint32_t word[SCAN_IT];
-#pragma unroll
-  for (int j = 0; j < SCAN_IT; j++) {
-    const unsigned wi = blk * SCAN_W + 32u * j + lane;
-    word[j] = wi < (unsigned)L.RW ? __ldcg(&row[wi]) : 0xFFFFFFFFu;
-  }
-  const float tdu = __ldg(&tdp[q]);
-  unsigned unew = 0;
-#pragma unroll
-  for (int j = 0; j < SCAN_IT; j++) {
-    const unsigned wi = blk * SCAN_W + 32u * j + lane;
-    uint32_t z = ~word[j], setm = 0;
-    while (z) {
-      const unsigned b = __ffs(z) - 1;
-      z &= z - 1;
-      const int x = mcol_pixel(L, wi * 32u + b);
-      if (x < 0) continue;
-      const unsigned pos = __ldg(&tinz[x]) & 0xFFFFu;
-      if (pos - q - 1u < szu) {  // x in the subtree of u: a new pair
-        setm |= 1u << b;
-        set_mark(a, x, ucol);
-        const float duv = __fsub_rn(__ldg(&tdp[pos]), tdu);
-        a.D[(size_t)u * N + x] = duv;
-        a.D[(size_t)x * N + u] = duv;
-        atomicAdd(&a.cnt[x], 1);
-        unew++;
-      }
-    }
-    if (setm) atomicOr(&row[wi], setm);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) unew += __shfl_xor_sync(0xffffffffu, unew, o);
-  if (lane == 0 && unew) atomicAdd(&a.cnt[u], (int)unew);
-  return lane == 0 ? unew : 0u;
-}
-
-// queue the big ancestors of a window whose chunk 0 this unit owns (mask
-// bigm, warp-uniform); rows that do not fit the queue are scanned in place
-__device__ __forceinline__ unsigned scan_push(const CommitArgs& a, int slot, ScanQ& SQ, unsigned bigm,
-                                              int q) {
-  const int lane = threadIdx.x & 31;
-  int base = lane == 0 ? atomicAdd(&SQ.n, __popc(bigm)) : 0;
-  base = __shfl_sync(0xffffffffu, base, 0);
-  unsigned lnew = 0;
-  while (bigm) {
-    const int ol = __ffs(bigm) - 1;
-    bigm &= bigm - 1;
-    if (base < SQ_CAP) {
-      if (lane == 0) SQ.q[base] = (uint16_t)(q + ol);
-    } else {
-      for (unsigned blk = 0; blk * SCAN_W < (unsigned)a.L.RW; blk++)
-        lnew += scan_row_part(a, slot, (unsigned)(q + ol), blk);
-    }
-    base++;
-  }
-  return lnew;
-}
-
 template <int U, bool VERIFY = false>
 __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int s, int p,
                                           unsigned long long* sim = nullptr, unsigned* ustat = nullptr,
-                                          bool corrupt = false, unsigned sb = 0xFFFFFFFFu,
-                                          ScanQ* SQ = nullptr) {
+                                          bool corrupt = false) {
   const int N = a.g.N;
   const int lane = threadIdx.x & 31;
   const int P = a.ts.nparts;
@@ -341,12 +242,7 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
     const int u_l = (int)(e_l & 0xFFFFu);
     // (verify mode tests full rows too: their pairs are all compared)
     const bool full_l = mych && u_l != s && !(VERIFY && a.verify) && __ldcg(&a.cnt[u_l]) >= N - 1;
-    const bool big_l = sz_l >= sb;  // row scan instead of chunks (queued by the owner of chunk 0)
-    unsigned work = __ballot_sync(0xffffffffu, mych && !full_l && !big_l);
-    if (SQ) {
-      const unsigned bigm = __ballot_sync(0xffffffffu, mych && !full_l && big_l && c0_l == 0);
-      if (bigm) total_new += scan_push(a, slot, *SQ, bigm, q);
-    }
+    unsigned work = __ballot_sync(0xffffffffu, mych && !full_l);
     while (work) {
       const int ol = __ffs(work) - 1;
       work &= work - 1;
@@ -519,7 +415,6 @@ __device__ __forceinline__ void fq_emit(FillQ& Q, int lane, bool open, int q, ui
 
 template <int G>
 __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot, int s, FillQ& Q,
-                                              ScanQ& SQ, int step,
                                               unsigned long long* sim = nullptr) {
   const int N = a.g.N;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -534,9 +429,6 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
   const unsigned long long t_a0 = sim ? gtimer() : 0ull;
   const MarkLayout L = a.L;
   unsigned lnew = 0;
-  // row-scan threshold of this step (written two steps ahead by the keeper; in
-  // flight with the partition words)
-  const unsigned sb = a.sbigv ? __ldcg(&a.sbigv[step]) : 0xFFFFFFFFu;
   // ---- phase A ----
   const uint32_t* part = a.ts.part + (size_t)slot * P;
   for (int k0 = wid; k0 < nu; k0 += 4 * nw) {
@@ -592,8 +484,7 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
     if (!tot) continue;
     if (!__shfl_sync(0xffffffffu, ok, 0)) {  // deep tree: fill these units in place
       for (int i = 0; i < 4; i++)
-        if (cn4[i]) lnew += fill_unit<(G > 4 ? 4 : G)>(a, slot, s, (int)blockIdx.x + (k0 + i * nw) * NB,
-                                                       nullptr, nullptr, false, sb, &SQ);
+        if (cn4[i]) lnew += fill_unit<(G > 4 ? 4 : G)>(a, slot, s, (int)blockIdx.x + (k0 + i * nw) * NB);
       continue;
     }
 #if GP_PHASEA_ANCHOR == 1
@@ -618,15 +509,9 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
     unsigned nop4[4], inc4[4], wt4[4], wsum = 0;
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-      const bool open_l = my4[i] && cv4[i] < N - 1;
-      const bool big_l = sz4[i] >= sb;
-      nop4[i] = (open_l && !big_l) ? my4[i] : 0u;
+      nop4[i] = (my4[i] && cv4[i] < N - 1) ? my4[i] : 0u;
       wt4[i] = fq_scan(lane, nop4[i], inc4[i]);
       wsum += wt4[i];
-      if (sb != 0xFFFFFFFFu) {
-        const unsigned bigm = __ballot_sync(0xffffffffu, open_l && big_l && c04[i] == 0);
-        if (bigm) lnew += scan_push(a, slot, SQ, bigm, (int)q4[i]);
-      }
     }
     int base = lane == 0 && wsum ? atomicAdd(&Q.n, (int)wsum) : 0;
     base = __shfl_sync(0xffffffffu, base, 0);
@@ -656,12 +541,7 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
         const unsigned take = fq_window(lane, qa, sz_l, 0u, count, mych, c0_l);
         const int u_l = (int)(e_l & 0xFFFFu);
         const bool full_l = mych && u_l != s && __ldcg(&a.cnt[u_l]) >= N - 1;
-        const bool big_l = sz_l >= sb;
-        fq_emit(Q, lane, mych && !full_l && !big_l, q, e_l, sz_l, c0_l, mych);
-        if (sb != 0xFFFFFFFFu) {
-          const unsigned bigm = __ballot_sync(0xffffffffu, mych && !full_l && big_l && c0_l == 0);
-          if (bigm) lnew += scan_push(a, slot, SQ, bigm, q);
-        }
+        fq_emit(Q, lane, mych && !full_l, q, e_l, sz_l, c0_l, mych);
         count -= take;
       }
     }
@@ -726,18 +606,6 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
       }
     }
     i0 = __shfl_sync(0xffffffffu, inext, 0);
-  }
-  // ---- phase C: row scans of the queued big ancestors ----
-  if (sb != 0xFFFFFFFFu) {
-    const unsigned nsq = (unsigned)min(*(volatile int*)&SQ.n, SQ_CAP);
-    const unsigned ipr = ((unsigned)L.RW + SCAN_W - 1u) / SCAN_W;  // items per row
-    const unsigned nit = nsq * ipr;
-    for (;;) {
-      unsigned it = lane == 0 ? (unsigned)atomicAdd(&SQ.head, 1) : 0u;
-      it = __shfl_sync(0xffffffffu, it, 0);
-      if (it >= nit) break;
-      lnew += scan_row_part(a, slot, SQ.q[it % nsq], it / nsq);
-    }
   }
   return lnew;
 }
@@ -921,7 +789,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   __shared__ unsigned long long red64[32];
   __shared__ int unit_ctr[2];  // per-CTA work-unit counters (alternating steps)
   __shared__ FillQ fq;         // per-CTA chunk queue (tree mode)
-  __shared__ ScanQ sq;         // per-CTA row-scan queue (tree mode, big ancestors)
   __shared__ uint32_t cand_s[CAND_CAP];  // candidate set: pixel | static key part << 16
   __shared__ unsigned long long sel_s;   // fast-path selection broadcast
   // candidate-set state, CTA-uniform (shared memory, not registers)
@@ -930,7 +797,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
   if (threadIdx.x == 0) {
     unit_ctr[0] = unit_ctr[1] = 0;
     fq.n = fq.res = fq.head = 0;
-    sq.n = sq.head = 0;
     cand_delta = use_cand ? max(1u, __ldcg(&a.ctl->cand_delta)) : 0u;
     cand_n = 0;  // valid set: 0 < cand_n <= CAND_CAP (a previous launch's set is not reused)
     cand_T = 0;
@@ -988,7 +854,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
     if (mode == 1) {
       lnew = fill_list(a, slot, s, lcur, ln, (!LEAN && a.dbgs) ? a.dbgs + (size_t)step * 8 : nullptr);
     } else if (LEAN || a.fillq) {
-      lnew = fill_tree_cta<G>(a, slot, s, fq, sq, step, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr);
+      lnew = fill_tree_cta<G>(a, slot, s, fq, a.dbgs ? a.dbgs + (size_t)step * 8 : nullptr);
     } else {
       // Work units of this tree are interleaved over the CTAs (unit = b + k *
       // nblocks) and pulled by the CTA's warps from a shared counter, so the
@@ -1031,10 +897,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
       atomicAdd(&a.dbgw[(size_t)step * 4 + 1], dt);
     }
     lnew = block_reduce_sum(lnew, red64);
-    if (threadIdx.x == 0) {  // all warps are past the fill
-      fq.n = fq.res = fq.head = 0;
-      sq.n = sq.head = 0;
-    }
+    if (threadIdx.x == 0) fq.n = fq.res = fq.head = 0;  // all warps are past the fill
     if (!LEAN && a.dbgw && threadIdx.x == 0) {
       const unsigned long long dt = gtimer() - tw0;
       atomicMax(&a.dbgw[(size_t)step * 4 + 2], dt);
@@ -1101,13 +964,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_commit(CommitArgs a) {
       if (mode == 0 && a.total_pairs - filled <= a.ctl->list_switch) f |= 1u;
       if (mode == 1 && live && (unsigned long long)dead * a.compact_div > live) f |= 2u;
       a.stepflags[step + 1] = f;
-      if (mode == 0 && a.sbigv) {
-        // row-scan threshold of step + 2: scan_mult4 / 4 x the mean unfilled
-        // columns per row, at least scan_min descendants (off above 65535)
-        const unsigned long long zbar = 2ull * (a.total_pairs - filled) / (unsigned long long)N;
-        const unsigned long long t = max((unsigned long long)a.scan_min, (zbar * a.scan_mult4) >> 2);
-        a.sbigv[step + 2] = t > 65535ull ? 0xFFFFFFFFu : (unsigned)t;
-      }
     }
     if (dbg) dbg[3] = gtimer();
     if (fast) {

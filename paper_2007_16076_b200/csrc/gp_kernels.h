@@ -131,9 +131,6 @@ struct CommitArgs {
   const int* ext;          // [N] pixel at each rank
   unsigned long long* selkey;  // [N+2] per-step packed selection (atomicMin target)
   unsigned* stepflags;     // [N+2] per-step decisions from the bookkeeping thread
-  unsigned* sbigv;         // [N+4] per-step row-scan threshold (descendants; ~0u: off); nullptr: off
-  unsigned scan_min;       // least subtree size scanned as a row
-  unsigned scan_mult4;     // threshold = scan_mult4 / 4 x mean unfilled columns per row
   int* seq;                // [N] committed sources
   unsigned long long* newp;// [N] new pairs per commit
   Ctl* ctl;
