@@ -1390,11 +1390,13 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
           CUDA_TRY(cudaEventRecord(rev[b], c->st4));
           return GP_OK;
         };
-        // log ranges whose copy has arrived: into the host array (row thread)
+        // log ranges whose copy has arrived: into the host array (row thread + helpers)
+        int patch_threads = 8;
+        if (const char* e = getenv("GP_E2E_PATCH_THREADS")) patch_threads = std::max(1, std::min(32, atoi(e)));
         auto drain_patches = [&]() {
           size_t done = 0;
           while (done < pchunks.size() && cudaEventQuery(pchunks[done].ev) == cudaSuccess) {
-            apply_patches(pchunks[done].b, pchunks[done].e, cut_n, 4);
+            apply_patches(pchunks[done].b, pchunks[done].e, cut_n, patch_threads);
             done++;
           }
           pchunks.erase(pchunks.begin(), pchunks.begin() + (long)done);
