@@ -951,7 +951,12 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     };
     if (nt <= 1 || n < 4096) { for (int t = 0; t < nt; t++) work(t); return; }
     std::vector<std::thread> th;
-    for (int t = 0; t < nt; t++) th.emplace_back(work, t);
+    int started = 0;
+    try {
+      for (; started < nt; started++) th.emplace_back(work, started);
+    } catch (...) {  // no more threads: the rest on this one
+    }
+    for (int t = started; t < nt; t++) work(t);
     for (auto& x : th) x.join();
   };
   if (D_host) {
@@ -1416,12 +1421,13 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
             cut_done = true;
             cut_n = hc.patch_n;
             patch_fetched = cut_n;
-            if (c->h_patch_cap < (size_t)cut_pairs + 1024) {  // at most one entry per pair still open
+            const size_t need = (size_t)(ca.total_pairs - hc.filled) + 1024;  // at most one entry per pair still open
+            if (c->h_patch_cap < need) {
               if (c->h_patch) cudaFreeHost(c->h_patch);
               c->h_patch = nullptr;
               c->h_patch_cap = 0;
-              CUDA_TRY(cudaHostAlloc(&c->h_patch, ((size_t)cut_pairs + 1024) * sizeof(uint2), cudaHostAllocDefault));
-              c->h_patch_cap = (size_t)cut_pairs + 1024;
+              CUDA_TRY(cudaHostAlloc(&c->h_patch, need * sizeof(uint2), cudaHostAllocDefault));
+              c->h_patch_cap = need;
             }
             if (int r = rs.enqueue(true, false)) return r;
             if (htime) fprintf(stderr, "[gp host] early send at round %d (step %d): %llu pairs left, log position %u, at %.1f ms\n",
@@ -1460,7 +1466,9 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
         CUDA_TRY(cudaGetDevice(&dev));
         const int cap_req = e2e_cap;
         e2e_cap = 0;  // (the worker requests the cap through want_cap)
-        std::thread worker([&] {
+        std::thread worker;
+        try {
+          worker = std::thread([&] {
           cudaSetDevice(dev);
           for (int idx = 0;; idx++) {
             while (idx >= nrounds.load(std::memory_order_acquire)) {
@@ -1472,7 +1480,10 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
             if (int r = process(idx)) { wrc.store(r); return; }
             if (cap_req > 0 && rs.open_rows >= 0 && rs.open_rows < N / 2) want_cap.store(cap_req);
           }
-        });
+          });
+        } catch (...) {
+          return fail(GP_EINTERNAL, "cannot start the row streaming thread");
+        }
         struct Joiner {  // every return path joins the worker
           std::thread& t;
           std::atomic<int>& stop;
