@@ -123,6 +123,8 @@ def test_fp32_zero_pixels_exact_heap(gp, oracle):
     {"GP_LIST_BATCH": "1", "GP_LIST_ALPHA": "6"}, {"GP_LIST_BATCH": "1", "GP_LIST_ALPHA": "6", "GP_LB_PACK_MIN": "0"},
     {"GP_LIST_BATCH": "1", "GP_COMPACT_DIV": "1"}, {"GP_LIST_BATCH": "1", "GP_CAND": "0"},
     {"GP_LIST_BATCH": "0"},
+    # two-sided tree fills (no transpose-merge pass)
+    {"GP_ONE_SIDED": "0"}, {"GP_ONE_SIDED": "0", "GP_LIST_BATCH": "1"},
 ])
 def test_tuning_knobs_do_not_change_results(gp, oracle, env, monkeypatch):
     img = np.random.default_rng(11).random((24, 20), dtype=np.float32)
@@ -173,6 +175,11 @@ def test_run_to_host_streams_the_same_array(gp, shape, kind, cap, cut, monkeypat
     if cut is not None:
         monkeypatch.setenv("GP_E2E_CUT", str(cut))
         monkeypatch.setenv("GP_LIST_BATCH", "1")
+    if cut == -1:  # also: two-sided fills, one round of lookahead
+        monkeypatch.setenv("GP_ONE_SIDED", "0")
+        monkeypatch.setenv("GP_E2E_LOOKAHEAD", "1")
+    if cut == 20000:  # also: the host-driven round loop (two-sided fills, rows sent at the end)
+        monkeypatch.setenv("GP_PIPELINE", "0")
 
     import torch
 
