@@ -420,10 +420,14 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int P = a.ts.nparts, NB = gridDim.x;
   const int nu = (P - (int)blockIdx.x + NB - 1) / NB;  // this CTA's units: blockIdx.x + k * NB
-  const size_t off = (size_t)slot * N;
-  const uint32_t* pre = a.ts.pre + off;
-  const uint16_t* szp = a.ts.szp + off;
-  const float* tdp = a.ts.tdp + off;
+  // 32-bit element indices into the tree store and the mark bitmap (slot * N
+  // + position < 2^32: slots < 65536, N <= 65536; row * RW + word < 2^27): one
+  // IMAD.WIDE per address instead of a 64-bit add chain -- the chunk loop is
+  // bound by the instructions it issues (profiles/r02_cfg5_k_commit_tree_late)
+  const unsigned off = (unsigned)slot * (unsigned)N;
+  const uint32_t* pre = a.ts.pre;
+  const uint16_t* szp = a.ts.szp;
+  const float* tdp = a.ts.tdp;
   const unsigned T = __ldg(&a.ts.T[slot]);
   const unsigned tq = T / (unsigned)P, tr = T % (unsigned)P;
   const unsigned long long t_a0 = sim ? gtimer() : 0ull;
@@ -465,8 +469,8 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
       sz4[i] = 0;
       e4[i] = 0;
       if (qa < N) {
-        sz4[i] = __ldg(&szp[qa]);
-        e4[i] = __ldg(&pre[qa]);
+        sz4[i] = __ldg(&szp[off + (unsigned)qa]);
+        e4[i] = __ldg(&pre[off + (unsigned)qa]);
       }
     }
     unsigned cn4[4], tot = 0;
@@ -535,8 +539,8 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
         unsigned sz_l = 0, mych, c0_l;
         uint32_t e_l = 0;
         if (qa < N) {
-          sz_l = __ldg(&szp[qa]);
-          e_l = __ldg(&pre[qa]);
+          sz_l = __ldg(&szp[off + (unsigned)qa]);
+          e_l = __ldg(&pre[off + (unsigned)qa]);
         }
         const unsigned take = fq_window(lane, qa, sz_l, 0u, count, mych, c0_l);
         const int u_l = (int)(e_l & 0xFFFFu);
@@ -567,7 +571,7 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
       const uint2 d = i0 + j < nq ? Q.desc[i0 + j] : make_uint2(0u, 0u);
       const bool v = i0 + j < nq && (unsigned)lane <= (d.y >> 27);
       const unsigned qb = d.y & 0xFFFFu, c = (d.y >> 16) & 0x7FFu;
-      ew[j] = v ? __ldg(&pre[qb + c * 32u + lane]) : 0u;
+      ew[j] = v ? __ldg(&pre[off + qb + c * 32u + (unsigned)lane]) : 0u;
       word[j] = v ? 0u : 0xFFFFFFFFu;
     }
     unsigned need = 0;  // bit j: lane still has to read the mark word of descriptor j
@@ -577,7 +581,7 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
     for (int j = 0; j < G; j++) {
       if ((need >> j) & 1u) {
         const int u = (int)(Q.desc[i0 + j].x & 0xFFFFu);
-        word[j] = ld_mark(a.mark + (size_t)u * L.RW + (ew[j] >> 21));
+        word[j] = ld_mark(a.mark + ((unsigned)u * (unsigned)L.RW + (ew[j] >> 21)));
       }
     }
 #pragma unroll
@@ -594,7 +598,7 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
           const unsigned qb = d.y & 0xFFFFu, c = (d.y >> 16) & 0x7FFu;
           set_mark(a, u, wcol);
           set_mark(a, w, ucol);
-          const float duv = __fsub_rn(__ldg(&tdp[qb + c * 32u + lane]), __ldg(&tdp[qb - 1]));
+          const float duv = __fsub_rn(__ldg(&tdp[off + qb + c * 32u + (unsigned)lane]), __ldg(&tdp[off + qb - 1u]));
           a.D[(size_t)u * N + w] = duv;
           if (!a.one_sided) a.D[(size_t)w * N + u] = duv;
           atomicAdd(&a.cnt[w], 1);
