@@ -329,8 +329,8 @@ __device__ __forceinline__ unsigned fill_unit(const CommitArgs& a, int slot, int
 //      different ancestors in flight together.
 // A unit that does not fit the queue's remaining room is filled in place by
 // fill_unit (deep trees).  Descriptor: x = pre entry of the ancestor u
-// (tile column << 16 | u); y = qb | chunk << 16 | (valid lanes - 1) << 27,
-// qb = preorder position of u's first descendant.
+// (tile column << 16 | u); y = preorder position of the chunk's first
+// descendant | valid lanes << 16.
 #ifndef GP_FQ_CAP
 #define GP_FQ_CAP 4096
 #endif
@@ -397,7 +397,7 @@ __device__ __forceinline__ void fq_write(FillQ& Q, int lane, unsigned base, unsi
     if (idx < total) {
       const unsigned c = c0 + (idx - ex);
       const unsigned nv = min(32u, sz - c * 32u);
-      Q.desc[base + idx] = make_uint2(eu, (unsigned)(q + ol + 1) | (c << 16) | ((nv - 1u) << 27));
+      Q.desc[base + idx] = make_uint2(eu, ((unsigned)(q + ol + 1) + c * 32u) | (nv << 16));
     }
   }
 }
@@ -568,10 +568,9 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
     uint32_t ew[G], word[G];
 #pragma unroll
     for (int j = 0; j < G; j++) {
-      const uint2 d = i0 + j < nq ? Q.desc[i0 + j] : make_uint2(0u, 0u);
-      const bool v = i0 + j < nq && (unsigned)lane <= (d.y >> 27);
-      const unsigned qb = d.y & 0xFFFFu, c = (d.y >> 16) & 0x7FFu;
-      ew[j] = v ? __ldg(&pre[off + qb + c * 32u + (unsigned)lane]) : 0u;
+      const unsigned dy = i0 + j < nq ? Q.desc[i0 + j].y : 0u;  // (no descriptor: no valid lane)
+      const bool v = (unsigned)lane < (dy >> 16);
+      ew[j] = v ? __ldg(&pre[off + (dy & 0xFFFFu) + (unsigned)lane]) : 0u;
       word[j] = v ? 0u : 0xFFFFFFFFu;
     }
     unsigned need = 0;  // bit j: lane still has to read the mark word of descriptor j
@@ -595,10 +594,11 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
         if (isnew) {
           const int w = (int)(ew[j] & 0xFFFFu);
           const uint32_t ucol = d.x >> 16;
-          const unsigned qb = d.y & 0xFFFFu, c = (d.y >> 16) & 0x7FFu;
           set_mark(a, u, wcol);
           set_mark(a, w, ucol);
-          const float duv = __fsub_rn(__ldg(&tdp[off + qb + c * 32u + (unsigned)lane]), __ldg(&tdp[off + qb - 1u]));
+          // (the ancestor's preorder position from its Euler word: new pairs are rare)
+          const unsigned qa = __ldg(&a.ts.tin[off + (unsigned)u]) & 0xFFFFu;
+          const float duv = __fsub_rn(__ldg(&tdp[off + (d.y & 0xFFFFu) + (unsigned)lane]), __ldg(&tdp[off + qa]));
           a.D[(size_t)u * N + w] = duv;
           if (!a.one_sided) a.D[(size_t)w * N + u] = duv;
           atomicAdd(&a.cnt[w], 1);
