@@ -134,6 +134,47 @@ def test_config_matches_golden(gp, index):
         assert h.hexdigest() == str(g["d_sha256"])
 
 
+@pytest.mark.parametrize("index", [4, 5])
+def test_config_through_run_to_host_matches_golden(gp, index):
+    """The e2e path at config scale: gp_run_to_host (one-sided tree fills completed at the
+    list switch, rows streamed, early bulk send, patch log) delivers the same bytes as the
+    golden array -- cfg4 (1 GiB, reference-pinned) and cfg5 (16 GiB, hashed in row blocks)."""
+    import ctypes
+
+    import torch
+
+    from paper_2007_16076_b200 import _lib
+
+    spec = CONFIGS[index]
+    g = load_golden(f"cfg{index}.npz")
+    img = make_image(index)
+    isf = spec.dtype == "f32"
+    L = _lib.lib()
+    n = spec.n
+    px = np.ascontiguousarray(img.astype(np.float32) if isf else img)
+    dtype = _lib.DTYPE_F32 if isf else _lib.DTYPE_U8
+    ctx, st = ctypes.c_void_p(), ctypes.c_void_p()
+    _lib.check(L.gp_ctx_create(spec.shape[0], spec.shape[1], dtype, _lib.ptr(px), 1, spec.conn, ctypes.byref(ctx)))
+    _lib.check(L.gp_store_create(n, ctypes.byref(st)))
+    try:
+        host = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+        seq = np.zeros(n, np.int32)
+        new = np.zeros(n, np.int64)
+        stats = _lib.RunStats()
+        _lib.check(L.gp_run_to_host(ctx, st, _lib.STRATEGY_FILLING_RATE, 0, 0, _lib.ptr(seq), _lib.ptr(new),
+                                    ctypes.byref(stats), ctypes.c_void_p(host.data_ptr())))
+        P = int(stats.raw_count)
+        assert P == int(g["raw"]) and np.array_equal(seq[:P], g["seq"]) and np.array_equal(new[:P], g["new"])
+        H = host.numpy()
+        h = hashlib.sha256()
+        for r0 in range(0, n, 2048):
+            h.update(np.ascontiguousarray(H[r0:r0 + 2048]).astype("<f4" if isf else "<i4").tobytes())
+        assert h.hexdigest() == str(g["d_sha256"])
+    finally:
+        L.gp_store_destroy(st)
+        L.gp_ctx_destroy(ctx)
+
+
 def test_api_known_answers(gp):
     img = gp.Image.from_flat(3, 1, [1, 2, 3])
     r = gp.propagate(img, gp.Metric.SUM, [0])
