@@ -789,6 +789,8 @@ static int ensure_tree_store(gp_ctx* c, int nparts) {
   CUDA_TRY(dalloc(&c->ts.tin, cap * N));
   c->ts.cap = (int)cap;
   c->ts.nparts = nparts;
+  // (the constant fits 32 bits above 1024 partitions)
+  c->ts.pmagic = (nparts > 1024 && nparts < (1 << 14)) ? (unsigned)(((1ull << 42) + (unsigned long long)nparts - 1) / (unsigned long long)nparts) : 0u;
   return GP_OK;
 }
 

@@ -444,8 +444,11 @@ __device__ __forceinline__ unsigned fill_tree_cta(const CommitArgs& a, int slot,
         const unsigned p = blockIdx.x + (unsigned)k * NB;
         hpw = __ldg(&part[p]);  // in flight with T
         // floor((p+1)T/P) - floor(pT/P) with T = tq*P + tr, in 32-bit arithmetic
-        hcnt = P < 65536 ? tq + ((p + 1) * tr) / (unsigned)P - (p * tr) / (unsigned)P
-                         : (unsigned)((((unsigned long long)p + 1) * T) / P - ((unsigned long long)p * T) / P);
+        // (P < 2^14: x / P == umulhi(x, ceil(2^42 / P)) >> 10 exactly for x < 2^28, and
+        // (p + 1) * tr < P^2 < 2^28 -- two multiplies instead of two 32-bit divisions)
+        hcnt = a.ts.pmagic ? tq + (__umulhi((p + 1) * tr, a.ts.pmagic) >> 10) - (__umulhi(p * tr, a.ts.pmagic) >> 10)
+             : P < 65536   ? tq + ((p + 1) * tr) / (unsigned)P - (p * tr) / (unsigned)P
+                           : (unsigned)((((unsigned long long)p + 1) * T) / P - ((unsigned long long)p * T) / P);
         if (!hcnt) hpw = 0;
       }
     }

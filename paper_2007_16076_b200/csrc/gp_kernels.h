@@ -27,6 +27,7 @@ struct TreeStore {
   uint32_t* C;  // ancestor/descendant pairs of the tree = sum of depths
   uint32_t* tin;  // per pixel: preorder position | descendant count << 16 (Euler interval)
   int nparts;  // commit warps (partition count)
+  unsigned pmagic;  // ceil(2^42 / nparts) when 1024 < nparts < 2^14 (exact x / nparts for x < 2^28), else 0
   int cap;     // slots
 };
 

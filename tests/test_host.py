@@ -70,3 +70,18 @@ def test_gaussian_matches_scipy():
     x = np.random.default_rng(3).standard_normal((30, 30))
     ref = nd.gaussian_filter(x, 2.0, mode="reflect", truncate=4.0)
     assert np.allclose(configs.gaussian_filter(x, 2.0), ref, atol=1e-12)
+
+
+def test_partition_magic_division_is_exact():
+    """commit.cu phase A: x / P == umulhi(x, ceil(2^42 / P)) >> 10 for x < 2^28 and P < 2^14
+    (the unit chunk counts floor((p+1)T/P) - floor(pT/P) without 32-bit divisions)."""
+    rng = np.random.default_rng(0)
+    for P in (1025, 2049, 4736, 9472, 14208, 16383):
+        M = ((1 << 42) + P - 1) // P
+        assert M < (1 << 32)  # the constant fits 32 bits above 1024 partitions (capi.cu uses it only there)
+        xs = np.concatenate([rng.integers(0, 1 << 28, 200_000, dtype=np.int64),
+                             np.arange(0, 4 * P, dtype=np.int64), (1 << 28) - 1 - np.arange(0, 4 * P, dtype=np.int64),
+                             (np.arange(1, 20_000, dtype=np.int64) * P) - 1, np.arange(1, 20_000, dtype=np.int64) * P])
+        xs = xs[(xs >= 0) & (xs < (1 << 28))]
+        q = ((xs.astype(object) * M) >> 32 >> 10).astype(np.int64)
+        assert np.array_equal(q, xs // P), P
