@@ -934,6 +934,7 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   RowStreamer rs{c, s, D_host, {}, 0};
   std::pair<uint2*, unsigned> patch_after_cut{nullptr, 0u};  // patch log and its position at the early send
   unsigned h_ctl_final_patch_n = 0;
+  std::vector<int>* g_waste_batch = nullptr;  // GP_DEBUG_WASTE
   struct PatchChunk { unsigned b, e; cudaEvent_t ev; };
   std::vector<PatchChunk> pchunks;  // log ranges copied to c->h_patch, not applied yet
   unsigned patch_fetched = 0;       // log position up to which the copy to the host is queued
@@ -1253,6 +1254,10 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
     }
     std::vector<EvPair> pev, cev;
     // one propagation batch on the propagation stream (host-driven loop)
+    const bool waste_dbg = getenv("GP_DEBUG_WASTE") != nullptr;
+    static thread_local std::vector<int> waste_batch;
+    waste_batch.assign(waste_dbg ? N : 0, -1);
+    if (waste_dbg) g_waste_batch = &waste_batch;
     auto batch = [&](int q) -> int {
       EvPair f;
       CUDA_TRY(evp.pair(f));
@@ -1263,6 +1268,14 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
       pev.push_back(f);
       S.batches++;
       S.kernels += 2;
+      if (waste_dbg) {  // GP_DEBUG_WASTE (host-driven loop): which batch propagated which pixel
+        CUDA_TRY(cudaStreamSynchronize(ps));
+        int nc = 0;
+        CUDA_TRY(cudaMemcpy(&nc, &d_ctl->ncand, 4, cudaMemcpyDeviceToHost));
+        std::vector<int> hc((size_t)std::max(nc, 1));
+        CUDA_TRY(cudaMemcpy(hc.data(), d_cands, (size_t)nc * 4, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < nc; i++) waste_batch[hc[i]] = (int)S.batches - 1;
+      }
       return GP_OK;
     };
     const bool pipelined = !debug && !(getenv("GP_PIPELINE") && !atoi(getenv("GP_PIPELINE")));
@@ -1739,6 +1752,21 @@ static int run_impl(gp_ctx* c, gp_store* s, int strategy, int naive_with_tree, i
   std::vector<unsigned long long> nw(P > 0 ? P : 1);
   if (P > 0) CUDA_TRY(cudaMemcpy(nw.data(), d_new, (size_t)P * 8, cudaMemcpyDeviceToHost));
   if (seq_out && P > 0) CUDA_TRY(cudaMemcpy(seq_out, d_seq, (size_t)P * 4, cudaMemcpyDeviceToHost));
+  if (g_waste_batch && P > 0) {  // GP_DEBUG_WASTE: propagated-but-never-committed trees per batch
+    std::vector<int> hs((size_t)P);
+    CUDA_TRY(cudaMemcpy(hs.data(), d_seq, (size_t)P * 4, cudaMemcpyDeviceToHost));
+    std::vector<char> committed((size_t)N, 0);
+    for (int i = 0; i < P; i++) committed[hs[i]] = 1;
+    std::vector<int> per((size_t)S.batches + 1, 0), tot((size_t)S.batches + 1, 0);
+    for (int v = 0; v < N; v++)
+      if ((*g_waste_batch)[v] >= 0) {
+        tot[(*g_waste_batch)[v]]++;
+        if (!committed[v]) per[(*g_waste_batch)[v]]++;
+      }
+    fprintf(stderr, "[gp waste] batch: trees wasted\n");
+    for (size_t b = 0; b < per.size(); b++)
+      if (tot[b]) fprintf(stderr, "[gp waste] %zu: %d %d\n", b, tot[b], per[b]);
+  }
   int64_t filled = 0;
   for (int i = 0; i < P; i++) {
     filled += (int64_t)nw[i];
