@@ -1087,7 +1087,14 @@ size_t prop_smem_bytes(int N) { return prop_layout(N, HIST_SMEM).total; }
 
 size_t prop_scratch_bytes(int N) { return align16(prop_layout(N, (size_t)N + 1).total); }
 
-bool prop_fits_smem(int N) { return prop_smem_bytes(N) <= 227 * 1024; }
+bool prop_fits_smem(int N) {
+  // Maps whose state needs more than half an SM's shared memory run the
+  // global-scratch variant (three 512-thread trees per SM) although one tree
+  // would fit: measured at 128x128, propagation 51.2 -> 43.2 ms (Voronoi u8)
+  // and 51.8 -> 46.6 ms (fp32, 4-connected).  GP_PROP_SMEM_KB overrides.
+  static const long cap_kb = getenv("GP_PROP_SMEM_KB") ? atol(getenv("GP_PROP_SMEM_KB")) : 113;
+  return prop_smem_bytes(N) <= (size_t)std::min(227l, std::max(0l, cap_kb)) * 1024;
+}
 
 // dynamic shared memory of one tree (CTA)
 static size_t prop_dyn_smem(int N) {
